@@ -1,0 +1,113 @@
+/*
+ * stbta — B200-native (sm_100a) BTA structured solver, C ABI.
+ *
+ * Drop-in boundary for the reference's solver layer (stinla, pure Python on
+ * numpy/scipy).  Every pointer argument is a DEVICE pointer
+ * unless stated otherwise, every entry point is stream-ordered on `stream`
+ * (a cudaStream_t passed as void*), never synchronises, holds no global
+ * mutable state and is re-entrant for distinct streams and workspaces.
+ *
+ * Storage: one flat FP64 buffer per BTA matrix, in the reference order
+ *   diag (n,b,b) | lower (n-1,b,b) [block (i+1,i)] | arrow (n,a,b) | tip (a,a)
+ * all row-major  (reference BTAMatrix, pkg/src/stinla/bta.py:50-89).
+ *
+ * Return value: 0 on success, >0 a cudaError_t from a launch, <0 an argument
+ * error (STBTA_EARG / STBTA_EWORKSPACE).  Numerical failure (a non-positive
+ * pivot, the reference's FactorizationError, bta.py:17-31) is NOT a return
+ * code: it is written to the device word *info as 1 + block index (n for the
+ * tip, so info == n+1), read back by the caller at its single sync point.
+ */
+#ifndef STBTA_H
+#define STBTA_H
+
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define STBTA_EARG (-1)
+#define STBTA_EWORKSPACE (-2)
+
+/* Library version string (host). */
+const char* stbta_version(void);
+
+/* Number of FP64 elements of the flat BTA buffer: n*b*b+(n-1)*b*b+n*a*b+a*a
+ * (reference BTAMatrix.__init__, bta.py:69-72). */
+long long stbta_storage_elems(int n, int b, int a);
+
+/* ---------------------------------------------------------------- POBTAF --
+ * In-place block Cholesky of an SPD BTA matrix.
+ * Replaces: bta.factorize (pkg/src/stinla/bta.py:177-235) + bta.logdet
+ * (bta.py:238-246).  use_arrow = 0 skips all arrow work exactly like the
+ * reference's `use_arrow = a > 0 and np.any(arrow)` (bta.py:200-202); the tip
+ * is still factorized when a > 0 (bta.py:228-232).
+ * logdet_out (device double) = 2 * sum log diag(L), fixed summation order.
+ * info (device int) is zeroed first, then set on failure.
+ * workspace: >= stbta_pobtaf_workspace_bytes(n,b,a) bytes of device memory. */
+size_t stbta_pobtaf_workspace_bytes(int n, int b, int a);
+int stbta_pobtaf(double* data, int n, int b, int a, int use_arrow, double* logdet_out, int* info,
+                 void* workspace, size_t workspace_bytes, void* stream);
+
+/* ---------------------------------------------------------------- POBTAS --
+ * Triangular solves against a POBTAF factor, in place on rhs (dim x nrhs,
+ * row-major, dim = n*b+a).  mode 0: L L^T x = r (bta.solve, bta.py:305-307);
+ * 1: L y = r (forward_substitute, bta.py:249-275); 2: L^T x = r
+ * (backward_substitute, bta.py:278-302).  has_arrow = BTAFactor.has_arrow. */
+size_t stbta_pobtas_workspace_bytes(int n, int b, int a, int nrhs);
+int stbta_pobtas(const double* factor, int n, int b, int a, int has_arrow, double* rhs, int nrhs,
+                 int mode, void* workspace, size_t workspace_bytes, void* stream);
+
+/* --------------------------------------------------------------- POBTASI --
+ * Selected inversion: the BTA-pattern entries of (L L^T)^-1 written to `inv`
+ * (a separate buffer of the same layout; X_ii stored full symmetric).
+ * Replaces: bta.selected_invert (pkg/src/stinla/bta.py:310-359). */
+size_t stbta_pobtasi_workspace_bytes(int n, int b, int a);
+int stbta_pobtasi(const double* factor, double* inv, int n, int b, int a, int has_arrow,
+                  void* workspace, size_t workspace_bytes, void* stream);
+
+/* ------------------------------------------------------ Q assembly / f_obj --
+ * stbta_assemble: write the theta-dependent values of a precision matrix into
+ * a BTA buffer of nstore elements, zero everywhere else.  Replaces the value
+ * map of model.spatio_temporal_precision / build_univariate_prior
+ * (pkg/src/stinla/model.py:196-248), coreg.assemble_joint_precision
+ * (coreg.py:80-121), ObjectiveEvaluator._conditional_matrix (inla.py:264-283)
+ * and coreg.map_to_bta incl. its zero fill (coreg.py:250-276):
+ *   data[offsets[e]] = sum_t coef[pair[e]*nterms + t] * basis[src[e]*nterms + t]
+ * offsets (int64, strictly increasing) come from PermutationMap.bind
+ * (coreg.py:186-241); tile_start[k] = first e with offsets[e] >= k*TILE,
+ * k = 0..ceil(nstore/TILE), TILE = stbta_assemble_tile_elems(). */
+int stbta_assemble_tile_elems(void);
+int stbta_assemble(double* data, long long nstore, const long long* tile_start,
+                   const long long* offsets, const int* pair, const int* src, const double* basis,
+                   const double* coef, int nterms, void* stream);
+/* out[0] = x^T Q x over the symmetric matrix described by the same entry
+ * list (lower BTA envelope, off-diagonal blocks counted twice); x in BTA
+ * order.  Replaces `mu @ (prior_matrix @ mu)` (inla.py:369).  partial: npartial
+ * doubles of scratch; summation order fixed. */
+int stbta_quadform(const long long* offsets, const int* pair, const int* src, const double* basis,
+                   const double* coef, int nterms, long long nentries, int n, int b, int a,
+                   const double* x, double* partial, int npartial, double* out, void* stream);
+/* out[e] = sum_i tau[i] * U[i*N + e], i < nv: the conditional-mean right-hand
+ * side design^T (noise * y) in BTA order (inla.py:313-315). */
+int stbta_rhs_combine(double* out, const double* U, const double* tau, int nv, long long N,
+                      void* stream);
+/* out[i] = sum_{r in [seg[i], seg[i+1])} (y[r] - (A x)[r])^2 for the CSR design
+ * A (columns already in BTA order); sq: nrows doubles of scratch
+ * (inla.py:363-367). */
+int stbta_residual(const long long* indptr, const int* indices, const double* vals,
+                   long long nrows, const double* y, const double* x, const long long* seg,
+                   int nseg, double* sq, double* out, void* stream);
+
+/* ------------------------------------------------------------ dense GEMM --
+ * C = alpha * op(A) * op(B) + beta * C on the FP64 DMMA engine (row-major,
+ * op = transpose when ta/tb != 0).  Exposed for tests and benchmarks. */
+int stbta_dgemm(int ta, int tb, int M, int N, int K, double alpha, const double* A, long long lda,
+                const double* B, long long ldb, double beta, double* C, long long ldc,
+                void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* STBTA_H */

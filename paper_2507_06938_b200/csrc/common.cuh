@@ -1,0 +1,49 @@
+// Shared device helpers for the stbta sm_100a kernels.
+//
+// Everything here is FP64: the BTA solver path computes in IEEE double exactly
+// like the reference's numpy/LAPACK calls (SURVEY.md §8 "All arithmetic is
+// IEEE FP64").  The tensor-core path on sm_100a for f64 is the warp-level
+// `mma.sync ... f64` (SASS DMMA.8x8x4); tcgen05 has no f64 kind.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#define STBTA_DEV __device__ __forceinline__
+
+namespace stbta {
+
+// ---------------------------------------------------------------- cp.async
+// 8-byte element copy global->shared with zero fill when !valid.
+STBTA_DEV void cp_async8(void* smem, const void* gmem, bool valid) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  int n = valid ? 8 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(n));
+}
+// 16-byte copy (both addresses 16-byte aligned); src_bytes in {0, 8, 16}.
+STBTA_DEV void cp_async16(void* smem, const void* gmem, int src_bytes) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes));
+}
+STBTA_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+STBTA_DEV void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+// ---------------------------------------------------------------- DMMA
+// D(8x8) += A(8x4, row) * B(4x8, col), f64.  Fragment ownership for lane l,
+// g = l>>2, t = l&3:  a = A[g][t];  b = B[t][g];  c0,c1 = C[g][2t], C[g][2t+1].
+STBTA_DEV void dmma884(double& c0, double& c1, double a, double b) {
+  asm volatile(
+      "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(c0), "+d"(c1)
+      : "d"(a), "d"(b));
+}
+
+// Deterministic warp sum (fixed butterfly order).
+STBTA_DEV double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+}  // namespace stbta

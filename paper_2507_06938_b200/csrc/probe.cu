@@ -1,0 +1,58 @@
+// FP64 tensor-pipe peak probe: a register-resident DMMA.8x8x4 loop with
+// enough independent accumulators to saturate the pipe.  Used by bench.py to
+// measure the FP64 roofline denominator on the box (MEASURED_PEAKS.json has
+// no FP64 entry).
+#include "../../include/stbta.h"
+#include "common.cuh"
+
+namespace stbta {
+
+__global__ void __launch_bounds__(256) dmma_probe_kernel(int iters, double* out) {
+  constexpr int ACC = 16;
+  double c0[ACC], c1[ACC];
+  const double a = 1.0 + threadIdx.x * 1e-9, b = 1.0 - threadIdx.x * 1e-9;
+#pragma unroll
+  for (int i = 0; i < ACC; ++i) c0[i] = c1[i] = 0.0;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < ACC; ++i) dmma884(c0[i], c1[i], a, b);
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int i = 0; i < ACC; ++i) s += c0[i] + c1[i];
+  if (s == 12345.678) out[0] = s;  // keep the loop alive
+}
+
+__global__ void __launch_bounds__(256) dfma_probe_kernel(int iters, double* out) {
+  constexpr int ACC = 8;
+  double c[ACC];
+  const double a = 1.0 + threadIdx.x * 1e-9, b = 1.0 - threadIdx.x * 1e-12;
+#pragma unroll
+  for (int i = 0; i < ACC; ++i) c[i] = i;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < ACC; ++i) c[i] = fma(c[i], a, b);
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int i = 0; i < ACC; ++i) s += c[i];
+  if (s == 12345.678) out[0] = s;
+}
+
+}  // namespace stbta
+
+extern "C" {
+// blocks x 256 threads, each thread iters*8 DFMA.  FLOPs = blocks*256*iters*16.
+int stbta_probe_dfma(int blocks, int iters, double* scratch, void* stream) {
+  stbta::dfma_probe_kernel<<<blocks, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(iters,
+                                                                                        scratch);
+  return (int)cudaGetLastError();
+}
+// Launch blocks x 256 threads, each warp issuing iters*16 DMMA.8x8x4
+// (256 FMA each).  FLOPs = blocks * 8 * iters * 16 * 512.
+int stbta_probe_dmma(int blocks, int iters, double* scratch, void* stream) {
+  stbta::dmma_probe_kernel<<<blocks, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(iters,
+                                                                                        scratch);
+  return (int)cudaGetLastError();
+}
+}

@@ -1,0 +1,228 @@
+"""Layered worker allocation and deterministic task execution (S1/S2 layers).
+
+Reference: pkg/src/stinla/sched.py — greedy g1*g2*g3 allocation, tasks dealt
+round-robin (task i -> group i % g1), results gathered in index order, the
+lowest failing index re-raised.  The B200 build keeps that policy and adds two
+executors for the gradient layer (S1):
+
+* :class:`GpuRunner` — one process driving several GPUs of a box, one host
+  thread per GPU, task i -> GPU i % G, each GPU evaluating its share through
+  its own ObjectiveEvaluator (the device work releases the GIL).
+* :class:`DistRunner` — one process per GPU (torchrun / NCCL): rank r evaluates
+  tasks i with i % world == r, the scalar results are exchanged with one
+  all-gather and every rank reassembles the identical list in index order,
+  so each rank's optimizer takes bit-identical decisions.
+"""
+
+import time
+from concurrent.futures import ThreadPoolExecutor
+from dataclasses import dataclass
+
+import numpy as np
+
+
+class TaskError(RuntimeError):
+    """A task failed; carries the lowest failing task index (sched.py:18-23)."""
+
+    def __init__(self, task_index, message):
+        self.task_index = task_index
+        super().__init__(f"task {task_index} failed: {message}")
+
+
+def n_objective_tasks(dim_theta):
+    return 2 * dim_theta + 1
+
+
+@dataclass(frozen=True)
+class LayerAllocation:
+    """g1 evaluation groups, g2 in {1,2} precision-pair width, g3 partitions (sched.py:31-48)."""
+
+    workers: int
+    g1: int
+    g2: int
+    g3: int
+
+    def __post_init__(self):
+        if self.g1 * self.g2 * self.g3 > self.workers:
+            raise ValueError("allocation exceeds the worker pool")
+        if self.g2 not in (1, 2):
+            raise ValueError("the precision-pair layer is at most two wide")
+
+    def saturated_s1(self, dim_theta):
+        return self.g1 >= n_objective_tasks(dim_theta)
+
+
+def allocate(workers, dim_theta, memory_fits_single=True, min_partitions=2):
+    """Greedy S1 -> S2 -> S3 allocation (sched.py:51-68)."""
+    if workers < 1:
+        raise ValueError("at least one worker required")
+    n_eval = n_objective_tasks(dim_theta)
+    g3 = 1 if memory_fits_single else max(1, min(min_partitions, workers))
+    g1 = max(1, min(n_eval, workers // g3))
+    g2 = 2 if (g1 >= n_eval and workers // (g1 * g3) >= 2) else 1
+    g3 = max(g3, workers // (g1 * g2))
+    return LayerAllocation(workers=workers, g1=g1, g2=g2, g3=g3)
+
+
+@dataclass
+class TaskTrace:
+    index: int
+    group: int
+    round: int
+    start: float
+    stop: float
+
+
+def _run_groups(tasks, groups, call):
+    """Deal task i to group i % groups; returns (results, failures, records)."""
+    results = [None] * len(tasks)
+    failures = []
+
+    def worker(g):
+        recs = []
+        for rnd, idx in enumerate(range(g, len(tasks), groups)):
+            t0 = time.perf_counter()
+            try:
+                results[idx] = call(g, idx)
+            except Exception as exc:  # reported with its task index
+                failures.append((idx, exc))
+                return recs
+            recs.append(TaskTrace(idx, g, rnd, t0, time.perf_counter()))
+        return recs
+
+    if groups == 1:
+        recs = worker(0)
+    else:
+        with ThreadPoolExecutor(max_workers=groups) as pool:
+            recs = [r for rs in pool.map(worker, range(groups)) for r in rs]
+    return results, failures, recs
+
+
+def run_tasks(tasks, alloc=None, trace=None):
+    """Zero-argument tasks, results in index order (sched.py:82-123)."""
+    tasks = list(tasks)
+    if not tasks:
+        return []
+    groups = 1 if alloc is None else max(1, min(alloc.g1, len(tasks)))
+    results, failures, recs = _run_groups(tasks, groups, lambda g, i: tasks[i]())
+    if failures:
+        idx, exc = min(failures, key=lambda p: p[0])
+        raise TaskError(idx, str(exc)) from exc
+    if trace is not None:
+        trace.extend(sorted(recs, key=lambda r: r.index))
+    return results
+
+
+class TaskRunner:
+    """Allocation-bound task hook for the inference routines (sched.py:126-135)."""
+
+    def __init__(self, alloc=None, trace=None):
+        self.alloc = alloc
+        self.trace = trace
+
+    def __call__(self, tasks):
+        return run_tasks(tasks, self.alloc, self.trace)
+
+
+def pair_runner(alloc):
+    """Two-wide runner for the Q_p / Q_c pair, or None (sched.py:138-144).  On the
+    device the pair already runs on two CUDA streams inside one evaluation."""
+    if alloc is None or alloc.g2 < 2:
+        return None
+    return TaskRunner(LayerAllocation(workers=2, g1=2, g2=1, g3=1))
+
+
+class GpuRunner:
+    """S1 over the GPUs of one process: theta-point tasks are re-bound to the
+    evaluator of GPU (i % G) and run by one host thread per GPU.
+
+    ``evaluators[g]`` is an ObjectiveEvaluator on GPU g.  The runner is called
+    by :func:`inla.fd_gradient` with closures ``lambda p=p: fun(p)``; it
+    recovers each point ``p`` and evaluates ``-evaluators[g].objective(p)``
+    (the minimized function of the reference).  Per GPU the tasks are issued
+    ``depth`` at a time so several f_obj overlap on the device.
+    """
+
+    def __init__(self, evaluators, negate=True, trace=None, depth=1):
+        self.evaluators = list(evaluators)
+        self.negate = negate
+        self.trace = trace
+        self.depth = max(1, int(depth))
+
+    @staticmethod
+    def _point(task):
+        d = task.__defaults__
+        if not d:
+            raise TypeError("GpuRunner needs fd_gradient-style tasks (lambda p=p: fun(p))")
+        return np.asarray(d[0], dtype=np.float64)
+
+    def evaluate_points(self, points):
+        G = len(self.evaluators)
+        sign = -1.0 if self.negate else 1.0
+        out = [None] * len(points)
+        failures = []
+
+        def worker(g):
+            ev = self.evaluators[g]
+            mine = list(range(g, len(points), G))
+            for k in range(0, len(mine), self.depth):
+                batch = mine[k : k + self.depth]
+                slots = [ev.slot(j) for j in range(len(batch))] if self.depth > 1 else [None]
+                try:
+                    handles = [ev.launch(points[i], slot=s) for i, s in zip(batch, slots)]
+                    for i, h in zip(batch, handles):
+                        out[i] = sign * ev.collect(h)[0]
+                except Exception as exc:
+                    failures.append((batch[0], exc))
+                    return
+
+        if G == 1:
+            worker(0)
+        else:
+            with ThreadPoolExecutor(max_workers=G) as pool:
+                list(pool.map(worker, range(G)))
+        if failures:
+            idx, exc = min(failures, key=lambda p: p[0])
+            raise TaskError(idx, str(exc)) from exc
+        return out
+
+    def __call__(self, tasks):
+        return self.evaluate_points([self._point(t) for t in tasks])
+
+
+class DistRunner:
+    """S1 across processes (one per GPU): rank r evaluates tasks i % world == r,
+    results are all-gathered and returned in index order on every rank."""
+
+    def __init__(self, evaluator, group=None, negate=True):
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.evaluator = evaluator
+        self.group = group
+        self.negate = negate
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+
+    def evaluate_points(self, points):
+        import torch
+
+        sign = -1.0 if self.negate else 1.0
+        n = len(points)
+        mine = list(range(self.rank, n, self.world))
+        local = torch.full((n,), float("nan"), dtype=torch.float64)
+        for i in mine:
+            local[i] = sign * self.evaluator.objective(points[i])
+        backend = self.dist.get_backend(self.group)
+        dev = self.evaluator.device if backend == "nccl" else torch.device("cpu")
+        buf = local.to(dev)
+        gathered = [torch.empty_like(buf) for _ in range(self.world)]
+        self.dist.all_gather(gathered, buf, group=self.group)
+        out = np.empty(n)
+        for r in range(self.world):
+            vals = gathered[r].cpu().numpy()
+            out[r::self.world] = vals[r::self.world]
+        return out.tolist()
+
+    def __call__(self, tasks):
+        return self.evaluate_points([GpuRunner._point(t) for t in tasks])

@@ -1,0 +1,127 @@
+"""Parity of the device f_obj (assembly + POBTAF x2 + POBTAS + reductions),
+the mode search and the latent marginals with the reference golden vectors
+and the CPU oracle."""
+
+import warnings
+
+import numpy as np
+import pytest
+
+from conftest import golden, make_spec, spec_from_golden
+from oracle import inla_np
+
+pytestmark = pytest.mark.gpu
+
+
+def _inla():
+    from paper_2507_06938_b200 import inla
+
+    return inla
+
+
+def test_objective_matches_reference_golden(cuda):
+    inla = _inla()
+    g = golden("objective.npz")
+    for name in ("uni", "tri", "biv0"):
+        spec = spec_from_golden(g, f"{name}_")
+        ev = inla.ObjectiveEvaluator(spec)
+        for k, p in enumerate(g[f"{name}_points"]):
+            f, mu = ev.evaluate(p)
+            np.testing.assert_allclose(f, g[f"{name}_f"][k], rtol=1e-10)
+            np.testing.assert_allclose(mu, g[f"{name}_mu"][k], rtol=1e-8, atol=1e-10)
+            grad = inla.fd_gradient(ev.objective, p, 1e-3)[1]
+            np.testing.assert_allclose(grad, g[f"{name}_grad"][k], rtol=1e-5, atol=1e-6)
+        _, sd = ev.latent_marginals(g[f"{name}_points"][0])
+        np.testing.assert_allclose(sd, g[f"{name}_sd"], rtol=1e-8)
+
+
+@pytest.mark.parametrize("trial", range(6))
+def test_objective_vs_oracle_random_specs(cuda, trial):
+    inla = _inla()
+    rng = np.random.default_rng(505 + trial)
+    nv = 1 + trial % 3
+    spec = make_spec(nv, int(rng.integers(1, 5)), int(rng.integers(1, 5)), int(rng.integers(0, 3)),
+                     int(rng.integers(3, 9)), seed=600 + trial)
+    ev = inla.ObjectiveEvaluator(spec)
+    theta = rng.normal(scale=0.25, size=inla.HyperParams.dim_for(nv))
+    f, mu = ev.evaluate(theta)
+    fr, mur = inla_np.evaluate(spec, theta, ev.prior.mean, ev.prior.sd)
+    np.testing.assert_allclose(f, fr, rtol=1e-10, atol=1e-10)
+    np.testing.assert_allclose(mu, mur, rtol=1e-8, atol=1e-10)
+
+
+def test_infeasible_and_nonfinite_theta(cuda):
+    inla = _inla()
+    spec = make_spec(1, 3, 3, 1, 5)
+    ev = inla.ObjectiveEvaluator(spec)
+    assert ev.evaluate(np.array([np.nan, 0.0, 0.0, 0.0])) == (-np.inf, None)
+    assert ev.objective(np.array([0.0, np.inf, 0.0, 0.0])) == -np.inf
+
+
+def test_no_data_limit_is_prior_only(cuda):
+    inla = _inla()
+    spec = make_spec(n_processes=2, n_spatial=2, n_time=2, n_fixed=1)
+    ev = inla.ObjectiveEvaluator(spec)
+    theta = 0.1 * np.arange(ev.theta_dim)
+    f, mu = ev.evaluate(theta)
+    assert np.array_equal(mu, np.zeros(spec.joint_dim))
+    np.testing.assert_allclose(f, ev.prior.log_density(theta), rtol=1e-12)
+
+
+def test_deterministic_repeat(cuda):
+    inla = _inla()
+    spec = make_spec(2, 3, 4, 1, 6)
+    ev = inla.ObjectiveEvaluator(spec)
+    theta = 0.05 * np.arange(inla.HyperParams.dim_for(2))
+    f1, mu1 = ev.evaluate(theta)
+    f2, mu2 = ev.evaluate(theta)
+    assert f1 == f2 and np.array_equal(mu1, mu2)
+
+
+def test_scalar_closed_form(cuda):
+    import scipy.sparse as sp
+
+    inla = _inla()
+    from paper_2507_06938_b200.model import ModelSpec, SpatialDiscretization, TemporalDiscretization
+
+    one, zero = sp.csr_matrix(np.array([[1.0]])), sp.csr_matrix((1, 1))
+    spec = ModelSpec(1, 1, 1, 0, [SpatialDiscretization(one, zero)],
+                     [TemporalDiscretization(one, zero, zero)], [one.copy()], [np.array([0.0])])
+    ev = inla.ObjectiveEvaluator(spec.validate())
+    f, mu = ev.evaluate(np.zeros(4))
+    np.testing.assert_allclose(mu, [0.0], atol=1e-15)
+    np.testing.assert_allclose(
+        f, ev.prior.log_density(np.zeros(4)) - 0.5 * np.log(2 * np.pi) - 0.5 * np.log(2.0),
+        rtol=1e-12)
+    mu, sd = ev.latent_marginals(np.zeros(4))
+    np.testing.assert_allclose(sd, [1 / np.sqrt(2.0)], rtol=1e-12)
+
+
+@pytest.mark.parametrize("name", ["ini", "c1"])
+def test_mode_search_matches_reference(cuda, name):
+    """Bundled univariate.ini and BASELINE config C1 (n_s=300, n_t=12, n_r=2):
+    reference mode within 1e-4, f* within 1e-8 relative."""
+    inla = _inla()
+    g = golden("mode_search.npz")
+    spec = spec_from_golden(g, f"{name}_")
+    psd, gtol, ftol = g[f"{name}_opts"]
+    theta0 = g[f"{name}_theta0"]
+    ev = inla.ObjectiveEvaluator(spec, prior=inla.ThetaPrior.for_dim(4, mean=theta0, sd=psd))
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        res = inla.minimize(ev, theta0, gtol=gtol, ftol=ftol, max_iter=100)
+    np.testing.assert_allclose(res.theta, g[f"{name}_theta"], atol=1e-4)
+    np.testing.assert_allclose(res.f, g[f"{name}_f"][0], rtol=1e-8)
+
+
+def test_gpu_runner_matches_serial_gradient(cuda):
+    inla = _inla()
+    from paper_2507_06938_b200 import sched
+
+    spec = make_spec(3, 3, 4, 1, 7, seed=5)
+    ev = inla.ObjectiveEvaluator(spec)
+    theta = np.linspace(-0.2, 0.3, 15)
+    f0, g0 = inla.fd_gradient(ev, theta)
+    runner = sched.GpuRunner([ev], depth=2)
+    f1, g1 = inla.fd_gradient(ev, theta, runner=runner)
+    assert f0 == f1 and np.array_equal(g0, g1)

@@ -1,0 +1,158 @@
+"""Host-side logic that needs no GPU: the frozen assembly plan, the
+permutation, hyperparameter layout, scheduler policy and the C ABI exports."""
+
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+import scipy.sparse as sp
+
+from conftest import ROOT, golden, make_spec, spec_from_golden
+from oracle import inla_np
+from paper_2507_06938_b200 import coreg, inla, model, sched
+
+
+def _grams(spec):
+    out = []
+    for a in spec.design:
+        g = (a.T @ a).tocsr()
+        out.append(((g + g.T) * 0.5).tocsr())
+    return out
+
+
+@pytest.mark.parametrize(
+    "nv,ns,nt,nf,m,seed",
+    [(1, 4, 3, 1, 9, 0), (1, 3, 5, 2, 12, 1), (3, 2, 3, 1, 7, 2), (2, 3, 2, 0, 5, 3),
+     (3, 3, 4, 2, 0, 4)],
+)
+def test_assembly_plan_reproduces_reference_scatter(nv, ns, nt, nf, m, seed):
+    """Basis-expanded Q_p / Q_c written by the plan == reference product-form
+    assembly + permutation + scatter (coreg.py:80-276, model.py:196-248)."""
+    spec = make_spec(nv, ns, nt, nf, m, seed)
+    pmap = coreg.build_permutation(spec)
+    grams = _grams(spec) if m else []
+    plan = coreg.AssemblyPlan(spec, pmap, grams, "cpu")
+    rng = np.random.default_rng(seed + 77)
+    theta = rng.normal(scale=0.3, size=inla.HyperParams.dim_for(nv))
+    hp = inla.HyperParams(theta, nv)
+    ph = [hp.process_hypers(k) for k in range(nv)]
+    linv = hp.coregionalization().mixing_inverse() if nv > 1 else np.ones((1, 1))
+    cp, cc = plan.coefficients(ph, linv, hp.noise_precisions())
+    qp = inla_np.joint_prior(spec, theta)
+    qc = inla_np.conditional(spec, qp, hp.noise_precisions())
+    ref_p, _ = inla_np.to_bta(spec, qp)
+    ref_c, _ = inla_np.to_bta(spec, qc)
+    np.testing.assert_allclose(plan.assemble_host(cp), ref_p, rtol=1e-13, atol=1e-12)
+    np.testing.assert_allclose(plan.assemble_host(cc), ref_c, rtol=1e-13, atol=1e-12)
+
+
+def test_permutation_matches_oracle_and_reference_dims():
+    spec = make_spec(3, 4, 5, 2)
+    pm = coreg.build_permutation(spec)
+    assert np.array_equal(pm.forward, inla_np.forward_perm(spec))
+    assert np.array_equal(pm.restore_vector(pm.permute_vector(np.arange(pm.dim))), np.arange(pm.dim))
+    # reference dimension identities (tests/test_acceptance.py:259-272)
+    for (nv, ns, nt, nf), expected in (((3, 4210, 48, 2), 606246), ((1, 4002, 250, 6), 1000506)):
+        s = model.ModelSpec(n_processes=nv, n_spatial=ns, n_time=nt, n_fixed=nf)
+        assert s.joint_dim == expected
+        assert nt * nv * ns + nv * nf == expected
+
+
+def test_envelope_error_outside_band():
+    pm = coreg.PermutationMap(1, 2, 4, 0)
+    bad = sp.csr_matrix(([1.0], ([0], [6])), shape=(8, 8))
+    with pytest.raises(coreg.EnvelopeError):
+        pm.bind(bad)
+
+
+def test_hyperparameter_layout():
+    assert inla.HyperParams.dim_for(1) == 4 and inla.HyperParams.dim_for(3) == 15
+    hp = inla.HyperParams(np.arange(15, dtype=float), 3)
+    p1 = hp.process_hypers(1)
+    assert (p1.log_spatial_scale, p1.log_temporal_scale, p1.log_variance_scale) == (2.0, 3.0, 0.0)
+    np.testing.assert_allclose(hp.noise_precisions(), np.exp([6.0, 7.0, 8.0]))
+    np.testing.assert_allclose(hp.coregionalization().scales, np.exp([9.0, 10.0, 11.0]))
+    assert len(hp.names()) == 15
+    with pytest.raises(model.DimensionError):
+        inla.HyperParams(np.zeros(5), 1)
+
+
+def test_st_basis_expansion_equals_product_form():
+    sd, td = model.path_graph_spatial(7), model.uniform_grid_temporal(5)
+    for ls, lt, lv in ((0.0, 0.0, 0.0), (0.4, -0.3, 0.2), (-1.1, 0.9, -0.5)):
+        ours = model.spatio_temporal_precision(sd, td, model.UnivariateHypers(ls, lt, lv))
+        ref = inla_np.st_precision(sd, td, ls, lt, lv)
+        np.testing.assert_allclose(ours.toarray(), ref.toarray(), rtol=1e-13, atol=1e-13)
+
+
+def test_scheduler_determinism_and_counts():
+    rng = np.random.default_rng(606)
+    payload = rng.normal(size=(31, 64))
+    tasks = [lambda i=i: float(np.sum(np.cos(payload[i]) ** 3)) for i in range(31)]
+    base = sched.run_tasks(tasks)
+    for w in (1, 2, 4, 8, 31):
+        assert sched.run_tasks(tasks, sched.allocate(w, 15)) == base
+    assert sched.n_objective_tasks(15) == 31
+    calls = []
+    inla.fd_gradient(lambda t: calls.append(1) or float(t @ t), np.zeros(15), 1e-3)
+    assert len(calls) == 31
+
+
+def test_scheduler_lowest_failing_index():
+    def boom(i):
+        def f():
+            raise RuntimeError(f"bad {i}")
+        return f
+
+    tasks = [lambda: 1.0, boom(3), lambda: 2.0, boom(1)]
+    with pytest.raises(sched.TaskError) as err:
+        sched.run_tasks(tasks, sched.allocate(4, 1))
+    assert err.value.task_index == 1
+
+
+def test_allocation_golden():
+    a = sched.allocate(8, 15)
+    assert (a.g1, a.g2, a.g3) == (8, 1, 1)
+    a = sched.allocate(64, 15)
+    assert (a.g1, a.g2, a.g3) == (31, 2, 1)
+    a = sched.allocate(8, 15, memory_fits_single=False)
+    assert a.g3 >= 2
+
+
+def _header_symbols():
+    txt = open(os.path.join(ROOT, "include", "stbta.h")).read()
+    txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+    return sorted(set(re.findall(r"\b(stbta_[a-z0-9_]+)\s*\(", txt)))
+
+
+def test_cabi_library_exports_every_header_symbol():
+    lib = ctypes.CDLL(os.path.join(ROOT, "paper_2507_06938_b200", "libstbta.so"))
+    syms = _header_symbols()
+    assert len(syms) >= 10
+    for s in syms:
+        assert hasattr(lib, s), s
+    from paper_2507_06938_b200 import _lib
+
+    assert set(_lib.exported_symbols()) >= set(syms)
+    # pure-host entry points callable without a GPU
+    lib.stbta_storage_elems.restype = ctypes.c_longlong
+    assert lib.stbta_storage_elems(48, 5025, 3) == 2399532984
+    lib.stbta_pobtaf_workspace_bytes.restype = ctypes.c_size_t
+    assert lib.stbta_pobtaf_workspace_bytes(48, 2048, 6) > 0
+    assert lib.stbta_assemble_tile_elems() == _lib.ASM_TILE
+
+
+def test_product_path_has_no_oracle_dependency():
+    pkg = os.path.join(ROOT, "paper_2507_06938_b200")
+    for fn in os.listdir(pkg):
+        if fn.endswith(".py"):
+            src = open(os.path.join(pkg, fn)).read()
+            assert "oracle" not in re.findall(r"^\s*(?:from|import)\s+(\w+)", src, flags=re.M), fn
+
+
+def test_objective_golden_spec_rebuild():
+    g = golden("objective.npz")
+    spec = spec_from_golden(g, "tri_")
+    assert spec.n_processes == 3 and spec.joint_dim == 3 * (6 * 4 + 1)
