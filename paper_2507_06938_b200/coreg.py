@@ -406,8 +406,9 @@ class AssemblyPlan:
                 for k in range(i, nv):
                     c = st_coefficients(process_hypers[k])
                     col = 0 if self.shared else 10 * k
-                    cp[p, col : col + ST_TERMS] += w[k, i, j] * c
-                    cp[p, col + TIP_TERM] += w[k, i, j] * spec.fixed_effect_precision
+                    with np.errstate(over="ignore", invalid="ignore"):
+                        cp[p, col : col + ST_TERMS] += w[k, i, j] * c
+                        cp[p, col + TIP_TERM] += w[k, i, j] * spec.fixed_effect_precision
         cc = cp.copy()
         if self.n_terms > self.gram_col0:
             for i in range(nv):
