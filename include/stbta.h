@@ -106,6 +106,16 @@ int stbta_dgemm(int ta, int tb, int M, int N, int K, double alpha, const double*
                 const double* B, long long ldb, double beta, double* C, long long ldc,
                 void* stream);
 
+/* ------------------------------------------------------- instrumentation --
+ * Kernel launches issued by this library since load (host counter; bench.py
+ * reports the difference over its timed region as gpu_launches). */
+long long stbta_launch_count(void);
+/* FP64 peak probes (bench.py's roofline denominator; MEASURED_PEAKS.json has
+ * no FP64 entry).  blocks x 256 threads; FLOPs = blocks*8*iters*16*512 for
+ * the DMMA.8x8x4 probe and blocks*256*iters*16 for the DFMA probe. */
+int stbta_probe_dmma(int blocks, int iters, double* scratch, void* stream);
+int stbta_probe_dfma(int blocks, int iters, double* scratch, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -41,6 +41,7 @@ _SIGNATURES = {
         c_int,
         [c_int, c_int, c_int, c_int, c_int, c_dbl, c_vp, c_ll, c_vp, c_ll, c_dbl, c_vp, c_ll, c_vp],
     ),
+    "stbta_launch_count": (c_ll, []),
     "stbta_probe_dmma": (c_int, [c_int, c_int, c_vp, c_vp]),
     "stbta_probe_dfma": (c_int, [c_int, c_int, c_vp, c_vp]),
     "stbta_assemble_tile_elems": (c_int, []),

@@ -82,10 +82,13 @@ class BTAMatrix:
             dev = torch.device(device) if device is not None else default_device()
             data = torch.zeros(total, dtype=torch.float64, device=dev)
         elif isinstance(data, torch.Tensor):
-            if data.dtype != torch.float64 or not data.is_cuda:
-                raise ValueError("device data must be a CUDA float64 tensor")
+            if data.dtype != torch.float64:
+                raise ValueError("data must be a float64 tensor")
             if data.numel() != total or data.dim() != 1 or not data.is_contiguous():
                 raise ValueError(f"data buffer must have {total} entries")
+            if not data.is_cuda:  # host tensor (pinned for an async upload): copied
+                dev = torch.device(device) if device is not None else default_device()
+                data = data.to(dev, non_blocking=data.is_pinned())
         else:
             arr = np.asarray(data, dtype=np.float64)
             if arr.shape != (total,):
@@ -119,8 +122,12 @@ class BTAMatrix:
         self._scatter_source = None
         return self
 
-    def numpy(self):
-        """Host copy of the flat buffer."""
+    def numpy(self, out=None):
+        """Host copy of the flat buffer; ``out`` may be a (pinned) CPU float64
+        tensor of the same size that receives the copy."""
+        if out is not None:
+            out.copy_(self.data)
+            return out.numpy()
         return self.data.detach().cpu().numpy()
 
     def to_dense(self):

@@ -13,6 +13,10 @@
 
 namespace stbta {
 
+// Host-side count of kernel launches issued by the library (bench.py's
+// gpu_launches; read with stbta_launch_count()).
+void count_launch();
+
 // ---------------------------------------------------------------- cp.async
 // 8-byte element copy global->shared with zero fill when !valid.
 STBTA_DEV void cp_async8(void* smem, const void* gmem, bool valid) {

@@ -209,6 +209,7 @@ static int launch_cfg(const GemmArgs& g, cudaStream_t stream) {
   const int vec_b = aligned16(g.B, two_b);
   dim3 grid(tiles_m * tiles_n, g.batch > 0 ? g.batch : 1);
   kern<<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, stream>>>(g, tiles_m, tiles_n, vec_a, vec_b);
+  count_launch();
   return (int)cudaGetLastError();
 }
 

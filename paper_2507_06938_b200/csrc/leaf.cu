@@ -139,6 +139,7 @@ __global__ void logdet_reduce_kernel(const double* slots, int count, double* out
 int launch_leaf(double* A, long long lda, int n, double* winv, double* ldslot, int* info, int code,
                 int mode, cudaStream_t st) {
   leaf_kernel<<<1, 256, 0, st>>>(A, lda, n, winv, ldslot, info, code, mode);
+  count_launch();
   return (int)cudaGetLastError();
 }
 
@@ -148,11 +149,13 @@ int launch_zero_upper(double* A, long long lda, int n, const int* info, cudaStre
   int blocks = (int)((total + 255) / 256);
   if (blocks > 148 * 8) blocks = 148 * 8;
   zero_upper_kernel<<<blocks, 256, 0, st>>>(A, lda, n, info);
+  count_launch();
   return (int)cudaGetLastError();
 }
 
 int launch_logdet_reduce(const double* slots, int count, double* out, cudaStream_t st) {
   logdet_reduce_kernel<<<1, 256, 0, st>>>(slots, count, out);
+  count_launch();
   return (int)cudaGetLastError();
 }
 

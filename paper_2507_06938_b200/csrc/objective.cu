@@ -177,6 +177,7 @@ int stbta_assemble(double* data, long long nstore, const long long* tile_start, 
   EntryTable t{offsets, pair, src, basis, coef, nterms};
   assemble_kernel<<<grid_for(ntiles, 1, 148 * 16), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
       data, nstore, tile_start, ntiles, t);
+  count_launch();
   return (int)cudaGetLastError();
 }
 
@@ -188,7 +189,9 @@ int stbta_quadform(const long long* offsets, const int* pair, const int* src, co
   EntryTable t{offsets, pair, src, basis, coef, nterms};
   const int g = grid_for(nentries, 256, npartial);
   quadform_kernel<<<g, 256, 0, st>>>(t, nentries, n, b, a, x, partial);
+  count_launch();
   ordered_sum_kernel<<<1, 32, 0, st>>>(partial, g, out);
+  count_launch();
   return (int)cudaGetLastError();
 }
 
@@ -196,6 +199,7 @@ int stbta_rhs_combine(double* out, const double* U, const double* tau, int nv, l
                       void* stream) {
   rhs_combine_kernel<<<grid_for(N, 256, 148 * 8), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
       out, U, tau, nv, N);
+  count_launch();
   return (int)cudaGetLastError();
 }
 
@@ -203,10 +207,15 @@ int stbta_residual(const long long* indptr, const int* indices, const double* va
                    const double* y, const double* x, const long long* seg, int nseg, double* sq,
                    double* out, void* stream) {
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  if (nrows > 0)
+  if (nrows > 0) {
     residual_kernel<<<grid_for(nrows, 256, 148 * 8), 256, 0, st>>>(indptr, indices, vals, nrows, y,
                                                                    x, sq);
-  if (nseg > 0) segment_sum_kernel<<<nseg, 32, 0, st>>>(sq, seg, nseg, out);
+    count_launch();
+  }
+  if (nseg > 0) {
+    segment_sum_kernel<<<nseg, 32, 0, st>>>(sq, seg, nseg, out);
+    count_launch();
+  }
   return (int)cudaGetLastError();
 }
 

@@ -20,7 +20,6 @@ namespace stbta {
 
 constexpr int CH = 64;     // chunk rows (== LEAF)
 constexpr int NRMAX = 8;   // right-hand sides per sweep launch
-constexpr int ARROW_MAX = 64;
 
 struct SweepArgs {
   const double* diag;
@@ -305,40 +304,37 @@ __global__ void __launch_bounds__(256) arrow_partial_kernel(SweepArgs p, double*
 }
 
 // mode 0 (forward): y_tip = L_tip^-1 (r_tip - sum_g partial[g]);  mode 1: x_tip = L_tip^-T y_tip.
-// Writes the tip segment of x and a packed copy xtip[a][NRMAX].
+// Works in place on the tip segment of x (any arrow size) and writes a packed
+// copy xtip[a][NRMAX] for the backward sweep's arrow coupling.
 __global__ void tip_solve_kernel(SweepArgs p, const double* partial, int nparts, double* xtip,
                                  int mode) {
   const int r = threadIdx.x;
   if (r >= p.ncols) return;
   const int a = p.a;
   const long long base = (long long)p.n * p.b;
-  double v[ARROW_MAX];
-  for (int t = 0; t < a; ++t) {
-    double s = p.x[(base + t) * p.ldx + r];
-    if (mode == 0 && p.has_arrow && partial != nullptr) {
+  double* v = p.x + base * p.ldx + r;  // v[t * ldx]
+  const long long ld = p.ldx;
+  if (mode == 0 && p.has_arrow && partial != nullptr) {
+    for (int t = 0; t < a; ++t) {
       double tot = 0.0;
       for (int g = 0; g < nparts; ++g) tot += partial[((long long)g * a + t) * NRMAX + r];
-      s -= tot;
+      v[t * ld] -= tot;
     }
-    v[t] = s;
   }
   if (mode == 0) {
     for (int t = 0; t < a; ++t) {
-      double s = v[t];
-      for (int u = 0; u < t; ++u) s -= p.tip[t * a + u] * v[u];
-      v[t] = s / p.tip[t * a + t];
+      double s = v[t * ld];
+      for (int u = 0; u < t; ++u) s -= p.tip[(long long)t * a + u] * v[u * ld];
+      v[t * ld] = s / p.tip[(long long)t * a + t];
     }
   } else {
     for (int t = a - 1; t >= 0; --t) {
-      double s = v[t];
-      for (int u = t + 1; u < a; ++u) s -= p.tip[u * a + t] * v[u];
-      v[t] = s / p.tip[t * a + t];
+      double s = v[t * ld];
+      for (int u = t + 1; u < a; ++u) s -= p.tip[(long long)u * a + t] * v[u * ld];
+      v[t * ld] = s / p.tip[(long long)t * a + t];
     }
   }
-  for (int t = 0; t < a; ++t) {
-    p.x[(base + t) * p.ldx + r] = v[t];
-    xtip[t * NRMAX + r] = v[t];
-  }
+  for (int t = 0; t < a; ++t) xtip[t * NRMAX + r] = v[t * ld];
 }
 
 static size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
@@ -357,7 +353,7 @@ static size_t pobtas_ws(int n, int b, int a, char* base, PobtasWs* o) {
   const size_t f = align_up((size_t)n * nck * sizeof(int));
   const size_t t = align_up(sizeof(int) * 2);
   const size_t pa = align_up((size_t)ARROW_PARTS * (a > 0 ? a : 1) * NRMAX * sizeof(double));
-  const size_t xt = align_up((size_t)ARROW_MAX * NRMAX * sizeof(double));
+  const size_t xt = align_up((size_t)(a > 0 ? a : 1) * NRMAX * sizeof(double));
   if (o) {
     o->flags = reinterpret_cast<int*>(base);
     o->ticket = reinterpret_cast<int*>(base + f);
@@ -377,6 +373,7 @@ static int run_sweeps(const SweepArgs& base_args, int mode, const PobtasWs& ws, 
     if ((e = (int)cudaMemsetAsync(p.flags, 0, fbytes, st))) return e;
     if ((e = (int)cudaMemsetAsync(p.ticket, 0, sizeof(int), st))) return e;
     fwd_sweep_kernel<<<total, 256, 0, st>>>(p);
+    count_launch();
     if ((e = (int)cudaGetLastError())) return e;
     if (p.a > 0) {
       int parts = 0;
@@ -385,20 +382,24 @@ static int run_sweeps(const SweepArgs& base_args, int mode, const PobtasWs& ws, 
         const int cpc = (int)((N + ARROW_PARTS - 1) / ARROW_PARTS);
         parts = (int)((N + cpc - 1) / cpc);
         arrow_partial_kernel<<<parts, 256, 0, st>>>(p, ws.partial, cpc);
+        count_launch();
         if ((e = (int)cudaGetLastError())) return e;
       }
       tip_solve_kernel<<<1, NRMAX, 0, st>>>(p, ws.partial, parts, ws.xtip, 0);
+      count_launch();
       if ((e = (int)cudaGetLastError())) return e;
     }
   }
   if (mode == 0 || mode == 2) {
     if (p.a > 0) {
       tip_solve_kernel<<<1, NRMAX, 0, st>>>(p, nullptr, 0, ws.xtip, 1);
+      count_launch();
       if ((e = (int)cudaGetLastError())) return e;
     }
     if ((e = (int)cudaMemsetAsync(p.flags, 0, fbytes, st))) return e;
     if ((e = (int)cudaMemsetAsync(p.ticket, 0, sizeof(int), st))) return e;
     bwd_sweep_kernel<<<total, 256, 0, st>>>(p, ws.xtip);
+    count_launch();
     if ((e = (int)cudaGetLastError())) return e;
   }
   return 0;
@@ -418,7 +419,7 @@ size_t stbta_pobtas_workspace_bytes(int n, int b, int a, int nrhs) {
 
 int stbta_pobtas(const double* factor, int n, int b, int a, int has_arrow, double* rhs, int nrhs,
                  int mode, void* workspace, size_t workspace_bytes, void* stream) {
-  if (factor == nullptr || rhs == nullptr || n < 1 || b < 1 || a < 0 || a > ARROW_MAX ||
+  if (factor == nullptr || rhs == nullptr || n < 1 || b < 1 || a < 0 ||
       nrhs < 1 || mode < 0 || mode > 2)
     return STBTA_EARG;
   if (workspace_bytes < stbta_pobtas_workspace_bytes(n, b, a, nrhs)) return STBTA_EWORKSPACE;

@@ -137,6 +137,7 @@ int stbta_pobtasi(const double* factor, double* inv, int n, int b, int a, int ha
     }
     // T1 = W^T - X_{i+1,i}^T L_{i+1,i} - X_{a,i}^T L_{a,i};  X_ii = T1 W
     transpose_kernel<<<tgrid, tblk, 0, st>>>(ws.W, b, ws.T1, b, b, nullptr);
+    count_launch();
     if ((e = (int)cudaGetLastError())) return e;
     if (sub && (e = gemm(st, true, false, ws.T1, b, Xl + i * bb, b, sub, b, b, b, b, -1.0, 1.0,
                          TRI_NONE, TRI_NONE)))

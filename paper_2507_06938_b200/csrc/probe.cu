@@ -5,7 +5,12 @@
 #include "../../include/stbta.h"
 #include "common.cuh"
 
+#include <atomic>
+
 namespace stbta {
+
+static std::atomic<long long> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 __global__ void __launch_bounds__(256) dmma_probe_kernel(int iters, double* out) {
   constexpr int ACC = 16;
@@ -42,6 +47,7 @@ __global__ void __launch_bounds__(256) dfma_probe_kernel(int iters, double* out)
 }  // namespace stbta
 
 extern "C" {
+long long stbta_launch_count(void) { return stbta::g_launches.load(); }
 // blocks x 256 threads, each thread iters*8 DFMA.  FLOPs = blocks*256*iters*16.
 int stbta_probe_dfma(int blocks, int iters, double* scratch, void* stream) {
   stbta::dfma_probe_kernel<<<blocks, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(iters,
