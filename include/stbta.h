@@ -113,6 +113,20 @@ long long stbta_launch_count(void);
 /* FP64 peak probes (bench.py's roofline denominator; MEASURED_PEAKS.json has
  * no FP64 entry).  blocks x 256 threads; FLOPs = blocks*8*iters*16*512 for
  * the DMMA.8x8x4 probe and blocks*256*iters*16 for the DFMA probe. */
+/* Debug hook: device buffer of 12 u64 into which POBTAF accumulates, per task
+ * kind (POTRF, TRSM, UPDATE, STRIP), {count, ns waiting, ns executing};
+ * NULL disables (the default). */
+void stbta_debug_set_profile(unsigned long long* buf);
+/* Debug micro-benchmark: `grid` CTAs each run `reps` tile products
+ * C_t -= A_t B_t^T (128x128, K=128) of CTA shape `variant`. */
+int stbta_debug_tile_bench(int variant, const double* A, const double* B, double* C, int ntile,
+                           int reps, int grid, void* stream);
+/* Debug micro-benchmark: `grid` CTAs each factorize + invert the SPD 128x128
+ * tile A `reps` times; ph (6 u64) receives CTA 0's phase times in ns. */
+int stbta_debug_potrf_bench(const double* A, double* out, int reps, int grid,
+                            unsigned long long* ph, void* stream);
+/* Debug: clock cycles of `iters` dependent DMMA (which=0) or DFMA (1) on one warp. */
+int stbta_debug_latency(int which, int iters, double* scratch, long long* cycles, void* stream);
 int stbta_probe_dmma(int blocks, int iters, double* scratch, void* stream);
 int stbta_probe_dfma(int blocks, int iters, double* scratch, void* stream);
 

@@ -1,4 +1,5 @@
-// POBTAF: in-place block Cholesky of an SPD BTA matrix (C ABI).
+// POBTAF: in-place block Cholesky of an SPD BTA matrix as ONE persistent
+// task-graph kernel (C ABI).
 //
 // Reference: bta.factorize (pkg/src/stinla/bta.py:177-235), per time block i
 //   diag[i]    = chol(diag[i])                                  (bta.py:206)
@@ -7,55 +8,477 @@
 //   tip       -= arrow[i] arrow[i]^T                             (222-227)
 // then tip = chol(tip) (bta.py:228-232), and logdet (bta.py:238-246).
 //
-// B200 mapping: the panel S_i = [lower[i]; arrow[i]] is one segmented operand,
-// so the TRSM is one recursive DMMA sweep over b + a rows and the Schur update
-// of [diag[i+1]; arrow[i+1]; tip] is ONE lower-triangular DMMA launch with
-// K = b.  Log-det partials are written per 64-leaf and summed once in a fixed
-// order; failures go to a device word, so the whole factorization is issued
-// without a host synchronisation.
+// B200 mapping.  The same elimination, refined to 128-wide panels of the
+// lower band (band.cuh), is a DAG of four task kinds:
+//   POTRF(s)        Cholesky + inverse W_s of diagonal tile s (one CTA)
+//   TRSM(s,R,q)     32-row strip q of tile (R,s) := strip W_s^T   (DMMA)
+//   UPDATE(s,R,C)   tile (R,C) -= X_R X_C^T, X = panel s tiles     (DMMA)
+//   STRIP(s,R,q)    lower part of strip q of diagonal tile (R,R)   (DMMA)
+// A persistent kernel (one CTA per SM) claims tasks from an atomic ticket in
+// a fixed topological order with one panel of look-ahead:
+//   P(0) U0(0) | P(1) Urest(0) U0(1) | P(2) Urest(1) U0(2) | ...
+// (U0 = updates of the next panel's column, Urest = the rest).  A task only
+// waits (acquire-spin on per-strip counters) for tasks with smaller tickets,
+// which are already running, so the schedule cannot deadlock; every tile is
+// updated in panel order, so results are bitwise deterministic.  A non-SPD
+// pivot sets info (1 + time block, n+1 for the tip) and an abort word that
+// drains the kernel.  Log-det partials per panel are summed in a fixed order.
+#include <cub/block/block_scan.cuh>
 #include <cstring>
 
 #include "../../include/stbta.h"
+#include "band.cuh"
+#include "potrf_tile.cuh"
 #include "stbta_internal.cuh"
+#include "tile_mma.cuh"
 
 namespace stbta {
 
-struct BtaView {
-  double *diag, *lower, *arrow, *tip;
-  int n, b, a;
-  explicit BtaView(double* data, int n_, int b_, int a_) : n(n_), b(b_), a(a_) {
-    const long long bb = (long long)b * b;
-    diag = data;
-    lower = diag + n * bb;
-    arrow = lower + (long long)(n - 1) * bb;
-    tip = arrow + (long long)n * a * b;
-  }
-  double* D(int i) const { return diag + (long long)i * b * b; }
-  double* Lo(int i) const { return lower + (long long)i * b * b; }
-  double* Ar(int i) const { return arrow + (long long)i * a * b; }
+constexpr int DAG_NT = 256;
+using Cfg128 = MmaCfg<128, 128, 64, 32, DAG_NT>;
+using Cfg32 = MmaCfg<32, 128, 32, 16, DAG_NT>;
+constexpr int TRSM_SMEM_DOUBLES = 32 * 132 + 128 * PT_LD + 4 * 32 * PT_WLD;
+constexpr int cmax(int x, int y) { return x > y ? x : y; }
+constexpr int DAG_SMEM_DOUBLES =
+    cmax(cmax(PT_SMEM_DOUBLES, TRSM_SMEM_DOUBLES), Cfg128::SMEM_DOUBLES);
+constexpr int W_SLOT = 4 * 32 * 32;  // per panel: the four W_kk^T blocks
+constexpr size_t DAG_SMEM_BYTES = DAG_SMEM_DOUBLES * sizeof(double);
+
+// Ticket order, six groups per panel s (critical chain first, then the bulk
+// of the previous panel, then this panel's remaining TRSMs and column s+1):
+//   G0 TRSM(s, s+1, q)          the next diagonal tile's strips   [critical]
+//   G1 STRIP(s-1, s+1, q)       previous panel's update of that tile
+//   G2 STRIP(s, s+1, q)         this panel's update of it  -> POTRF(s+1)
+//   G3 E(s-1) \ G1              bulk updates of panel s-1, columns >= s+1
+//   G4 TRSM(s, R, q), R > s+1
+//   G5 UPDATE(s, R, s+1), R > s+1
+// Every task depends only on tasks of earlier groups (or the panel worker's
+// POTRF, which depends only on earlier groups), so ticket order is a
+// topological order and spinning never deadlocks.
+enum { T_POTRF = 0, T_TRSM = 1, T_UPD = 2, T_STRIP = 3 };
+constexpr int NGRP = 6;
+struct DagWs {
+  int* gstart;   // G + 1 group starts
+  int* ctr;      // dependency counters
+  double* W;     // S slots of W_SLOT doubles (diagonal-block inverses)
+  double* slots; // S log-det partials
+  int* ticket;
+  int* abort_flag;
+  int* role;     // first CTA to arrive becomes the panel (POTRF) worker
+  int G;
+  unsigned long long* prof;  // optional: per task type {count, wait ns, exec ns}
 };
+
+STBTA_DEV unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+// does panel p = s-1 update tile (s+1, s+1)?  (then G1(s) holds its strips)
+STBTA_DEV bool g1_active(const Band& g, int s) {
+  if (s < 1) return false;
+  int mb;
+  const int mp = band_rows(g, s - 1, &mb);
+  return mp >= 2 && band_row(g, s - 1, 1, mb) == s + 1;
+}
+
+STBTA_DEV int group_size(const Band& g, int kind, int s) {
+  int mb;
+  const int m = band_rows(g, s, &mb);
+  switch (kind) {
+    case 0: return m >= 1 ? NSTRIP : 0;
+    case 1: return g1_active(g, s) ? NSTRIP : 0;
+    case 2: return m >= 1 ? NSTRIP : 0;
+    case 3: {
+      if (s < 1) return 0;
+      const int mp = band_rows(g, s - 1, &mb);
+      const int e = mp >= 2 ? NSTRIP * (mp - 1) + (mp - 1) * (mp - 2) / 2 : 0;
+      return e - (g1_active(g, s) ? NSTRIP : 0);
+    }
+    case 4: return m >= 1 ? NSTRIP * (m - 1) : 0;
+    default: return m >= 1 ? m - 1 : 0;
+  }
+}
+
+inline int n_groups(int S) { return NGRP * S; }
+
+// one CTA of 1024 threads: gstart[gi] = sum of sizes of groups < gi
+__global__ void __launch_bounds__(1024) dag_setup_kernel(Band g, DagWs ws) {
+  using Scan = cub::BlockScan<int, 1024>;
+  __shared__ typename Scan::TempStorage tmp;
+  __shared__ int carry;
+  const int G = ws.G;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int base = 0; base < G; base += 1024) {
+    const int gi = base + threadIdx.x;
+    int sz = 0;
+    if (gi < G) sz = group_size(g, gi % NGRP, gi / NGRP);
+    int ex, tot;
+    Scan(tmp).ExclusiveSum(sz, ex, tot);
+    if (gi < G) ws.gstart[gi] = carry + ex;
+    __syncthreads();
+    if (threadIdx.x == 0) carry += tot;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) ws.gstart[G] = carry;
+}
+
+struct Task {
+  int type, s, R, C, q;
+};
+
+STBTA_DEV Task decode(const Band& g, const DagWs& ws, int t) {
+  int lo = 0, hi = ws.G;  // gstart[lo] <= t < gstart[hi]
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (__ldg(ws.gstart + mid) <= t) lo = mid; else hi = mid;
+  }
+  const int kind = lo % NGRP, s = lo / NGRP;
+  int local = t - __ldg(ws.gstart + lo);
+  Task k{};
+  switch (kind) {
+    case 0: k.type = T_TRSM; k.s = s; k.R = s + 1; k.q = local; return k;
+    case 1: k.type = T_STRIP; k.s = s - 1; k.R = k.C = s + 1; k.q = local; return k;
+    case 2: k.type = T_STRIP; k.s = s; k.R = k.C = s + 1; k.q = local; return k;
+    case 4: {
+      int mb;
+      band_rows(g, s, &mb);
+      k.type = T_TRSM; k.s = s; k.R = band_row(g, s, 1 + local / NSTRIP, mb); k.q = local % NSTRIP;
+      return k;
+    }
+    case 5: {
+      int mb;
+      band_rows(g, s, &mb);
+      k.type = T_UPD; k.s = s; k.R = band_row(g, s, 1 + local, mb); k.C = s + 1;
+      return k;
+    }
+    default: break;
+  }
+  // G3: E(p), p = s-1, columns j = 1..mp-1; column 1's strips are in G1 when active
+  const int p = s - 1;
+  int mb;
+  const int mp = band_rows(g, p, &mb);
+  const bool skip = g1_active(g, s);
+  k.s = p;
+  for (int j = 1; j < mp; ++j) {
+    const int ns = (j == 1 && skip) ? 0 : NSTRIP;
+    const int cnt = ns + (mp - 1 - j);
+    if (local < cnt) {
+      const int c = band_row(g, p, j, mb);
+      if (local < ns) { k.type = T_STRIP; k.R = k.C = c; k.q = local; return k; }
+      k.type = T_UPD;
+      k.R = band_row(g, p, j + 1 + (local - ns), mb);
+      k.C = c;
+      return k;
+    }
+    local -= cnt;
+  }
+  k.type = -1;  // unreachable
+  return k;
+}
+
+STBTA_DEV int need(const Band& g, int R, int C) { return n_updates(g, R, C, C); }
+
+// The panel worker: POTRF(s) for s = 0..S-1 in order, on one dedicated CTA
+// (its instruction cache stays warm with the factorization code, and the
+// panel chain never queues behind bulk updates).  Returns false on abort.
+STBTA_DEV bool potrf_worker(const Band& g, const DagWs& ws, int* info, double* smem) {
+  __shared__ int s_ok, s_fail;
+  __shared__ double s_logdet;
+  const int tid = threadIdx.x;
+  const int NB = g.n * g.nbt;
+  for (int s = 0; s < g.S; ++s) {
+    const int w = tile_extent(g, s);
+    unsigned long long t0 = 0, t1 = 0;
+    if (ws.prof != nullptr && tid == 0) t0 = gtimer();
+    if (tid == 0) { s_ok = 1; s_fail = 0; }
+    __syncthreads();
+    if (tid < NSTRIP && !spin_geq(counter(g, ws.ctr, s, tid, s), need(g, s, s), ws.abort_flag)) s_ok = 0;
+    __syncthreads();
+    if (!s_ok) return false;
+    if (ws.prof != nullptr && tid == 0) t1 = gtimer();
+    {
+      double* T = smem;
+      double* WT = T + 128 * PT_LD;
+      double* scratch = WT + 4 * 32 * PT_WLD;
+      const TilePtr tp = tile_ptr(g, s, s);
+      {
+        const int warp = tid >> 5, lane = tid & 31;
+        for (int r = warp; r < w; r += DAG_NT / 32) {
+          const double* src = tp.p + (long long)r * tp.ld;
+          for (int c = lane; c <= r; c += 32) cp_async8(T + r * PT_LD + c, src + c, true);
+        }
+      }
+      cp_async_commit();
+      if (w < 128) {  // identity padding of a partial tile
+        for (int e = tid; e < 128 * 128; e += DAG_NT) {
+          const int r = e >> 7, c = e & 127;
+          if (r >= w || c >= w) T[r * PT_LD + c] = (r == c) ? 1.0 : 0.0;
+        }
+      }
+      cp_async_wait<0>();
+      __syncthreads();
+      unsigned long long ph[4] = {0, 0, 0, 0};
+      const unsigned long long tl = (ws.prof && tid == 0) ? gtimer() : 0;
+      const int fail = potrf_tile_smem<DAG_NT>(T, WT, scratch, &s_logdet, &s_fail,
+                                               ws.prof ? ph : nullptr);
+      if (fail) {
+        if (tid == 0) {
+          const int code = (s < NB) ? 1 + s / g.nbt : 1 + g.n;
+          atomicCAS(info, 0, code);
+          __threadfence();
+          atomicExch(ws.abort_flag, 1);
+        }
+        return false;
+      }
+      // L (zero strict upper) back to the tile, W_kk^T blocks to the panel's slot
+      {
+        const int warp = tid >> 5, lane = tid & 31;
+        for (int r = warp; r < w; r += DAG_NT / 32) {
+          double* dst = tp.p + (long long)r * tp.ld;
+          for (int c = lane; c < w; c += 32) dst[c] = (c <= r) ? T[r * PT_LD + c] : 0.0;
+        }
+      }
+      double* Wg = ws.W + (long long)s * W_SLOT;
+      for (int e = tid; e < W_SLOT; e += DAG_NT) {
+        const int kb = e >> 10, c = (e >> 5) & 31, i = e & 31;
+        Wg[e] = WT[kb * 32 * PT_WLD + c * PT_WLD + i];
+      }
+      if (tid == 0) ws.slots[s] = s_logdet;
+      __syncthreads();
+      if (ws.prof && tid == 0) {
+        const unsigned long long te = gtimer();
+        for (int k = 0; k < 3; ++k) atomicAdd(ws.prof + 12 + k, ph[k]);
+        atomicAdd(ws.prof + 16, (te - tl) - (ph[0] + ph[1] + ph[2]));
+        atomicAdd(ws.prof + 17, tl - t1);
+      }
+      if (tid == 0) {
+        __threadfence();
+        for (int q = 0; q < NSTRIP; ++q) atomicAdd(counter(g, ws.ctr, s, q, s), 1);
+        if (ws.prof) {
+          atomicAdd(ws.prof + 0, 1ull);
+          atomicAdd(ws.prof + 1, t1 - t0);
+          atomicAdd(ws.prof + 2, gtimer() - t1);
+        }
+      }
+    }
+    __syncthreads();
+  }
+  return true;
+}
+
+__global__ void __launch_bounds__(DAG_NT, 1) pobtaf_dag_kernel(Band g, DagWs ws, int* info) {
+  extern __shared__ __align__(16) double smem[];
+  __shared__ int s_ticket, s_ok;
+  __shared__ Task s_task;
+  const int tid = threadIdx.x;
+  const int total = ws.gstart[ws.G];
+  const int NB = g.n * g.nbt;
+  __shared__ int s_role;
+  if (tid == 0) s_role = atomicAdd(ws.role, 1);
+  __syncthreads();
+  if (s_role == 0) {
+    potrf_worker(g, ws, info, smem);
+    return;
+  }
+
+  for (;;) {
+    if (tid == 0) {
+      const int t = atomicAdd(ws.ticket, 1);
+      s_ticket = t;
+      if (t < total) s_task = decode(g, ws, t);
+      s_ok = 1;
+    }
+    __syncthreads();
+    if (s_ticket >= total) break;
+    const Task tk = s_task;
+    const int s = tk.s;
+    const int w = tile_extent(g, s);  // panel width = K of every product
+    unsigned long long t0 = 0, t1 = 0;
+    if (ws.prof != nullptr && tid == 0) t0 = gtimer();
+
+    // ------------------------------------------------------ dependencies
+    {
+      const int* p = nullptr;
+      int target = 0;
+      if (tk.type == T_TRSM) {
+        if (tid < NSTRIP) { p = counter(g, ws.ctr, s, tid, s); target = need(g, s, s) + 1; }
+        else if (tid == NSTRIP) { p = counter(g, ws.ctr, tk.R, tk.q, s); target = need(g, tk.R, s); }
+      } else if (tk.type == T_UPD) {
+        if (tid < NSTRIP) { p = counter(g, ws.ctr, tk.R, tid, s); target = need(g, tk.R, s) + 1; }
+        else if (tid < 2 * NSTRIP) { p = counter(g, ws.ctr, tk.C, tid - NSTRIP, s); target = need(g, tk.C, s) + 1; }
+        else if (tid < 3 * NSTRIP) { p = counter(g, ws.ctr, tk.R, tid - 2 * NSTRIP, tk.C); target = n_updates(g, tk.R, tk.C, s); }
+      } else {  // T_STRIP
+        if (tid <= tk.q) { p = counter(g, ws.ctr, tk.R, tid, s); target = need(g, tk.R, s) + 1; }
+        else if (tid == NSTRIP) { p = counter(g, ws.ctr, tk.R, tk.q, tk.R); target = n_updates(g, tk.R, tk.R, s); }
+      }
+      if (p != nullptr && !spin_geq(p, target, ws.abort_flag)) s_ok = 0;
+      __syncthreads();
+      if (!s_ok) break;
+    }
+    if (ws.prof != nullptr && tid == 0) t1 = gtimer();
+
+    // ------------------------------------------------------ execute
+    if (tk.type == T_TRSM) {
+      const int ext = tile_extent(g, tk.R);
+      const int r0 = tk.q * TS;
+      const int rows = min(TS, ext - r0);
+      if (rows > 0) {
+        constexpr int XLD = 132;
+        double* X = smem;                 // 32 x XLD
+        double* Ls = X + 32 * XLD;        // 128 x PT_LD (strictly lower blocks used)
+        double* WT = Ls + 128 * PT_LD;    // 4 x 32 x PT_WLD
+        const TilePtr xp = tile_ptr(g, tk.R, s);
+        const TilePtr lp = tile_ptr(g, s, s);
+        double* Xg = xp.p + (long long)r0 * xp.ld;
+        for (int e = tid; e < 32 * 128; e += DAG_NT) {
+          const int r = e >> 7, c = e & 127;
+          if (r < rows && c < w) cp_async8(X + r * XLD + c, Xg + (long long)r * xp.ld + c, true);
+          else X[r * XLD + c] = 0.0;
+        }
+        for (int e = tid; e < 128 * 128; e += DAG_NT) {
+          const int r = e >> 7, c = e & 127;
+          if ((r >> 5) > (c >> 5)) {  // strictly-lower 32-blocks
+            if (r < w && c < w) cp_async8(Ls + r * PT_LD + c, lp.p + (long long)r * lp.ld + c, true);
+            else Ls[r * PT_LD + c] = 0.0;
+          }
+        }
+        const double* Wg = ws.W + (long long)s * W_SLOT;
+        for (int e = tid; e < W_SLOT; e += DAG_NT) {
+          const int kb = e >> 10, c = (e >> 5) & 31, i = e & 31;
+          cp_async8(WT + kb * 32 * PT_WLD + c * PT_WLD + i, Wg + e, true);
+        }
+        cp_async_commit();
+        cp_async_wait<0>();
+        __syncthreads();
+        trsm_strip_smem<DAG_NT, XLD>(X, Ls, WT, w);
+        for (int e = tid; e < rows * w; e += DAG_NT) {
+          const int r = e / w, c = e - r * w;
+          Xg[(long long)r * xp.ld + c] = X[r * XLD + c];
+        }
+        const bool same_block = (tk.R < NB) ? (s < NB && tk.R / g.nbt == s / g.nbt) : (s >= NB);
+        if (same_block) {
+          // clear the mirrored strict-upper strip of the diagonal block / tip
+          const TilePtr up = tile_ptr_upper(g, tk.R, s);
+          for (int e = tid; e < w * rows; e += DAG_NT) {
+            const int r = e / rows, c = e % rows;
+            up.p[(long long)r * up.ld + r0 + c] = 0.0;
+          }
+        }
+      }
+      __syncthreads();
+      if (tid == 0) {
+        __threadfence();
+        atomicAdd(counter(g, ws.ctr, tk.R, tk.q, s), 1);
+      }
+    } else if (tk.type == T_UPD) {
+      const TilePtr rp = tile_ptr(g, tk.R, s);
+      const TilePtr cp = tile_ptr(g, tk.C, s);
+      const TilePtr tp = tile_ptr(g, tk.R, tk.C);
+      const int er = tile_extent(g, tk.R), ec = tile_extent(g, tk.C);
+      double acc[Cfg128::MF][Cfg128::NF][2];
+      acc_load<Cfg128>(acc, tp.p, tp.ld, er, ec, 0, 0);
+      const Opnd A{rp.p, rp.ld, er, rp.vec};
+      const Opnd B{cp.p, cp.ld, ec, cp.vec};
+      tile_mma<Cfg128, true>(acc, A, B, w, 128, smem);
+      acc_store<Cfg128>(acc, tp.p, tp.ld, er, ec, 0, 0, 0, 1.0);
+      __syncthreads();
+      if (tid == 0) {
+        __threadfence();
+        for (int q = 0; q < NSTRIP; ++q) atomicAdd(counter(g, ws.ctr, tk.R, q, tk.C), 1);
+      }
+    } else {  // T_STRIP
+      const int ext = tile_extent(g, tk.R);
+      const int r0 = tk.q * TS;
+      const int rows = min(TS, ext - r0);
+      if (rows > 0) {
+        const TilePtr xp = tile_ptr(g, tk.R, s);
+        const TilePtr tp = tile_ptr(g, tk.R, tk.R);
+        const int ncol = min(r0 + TS, ext);
+        double acc[Cfg32::MF][Cfg32::NF][2];
+        acc_load<Cfg32>(acc, tp.p + (long long)r0 * tp.ld, tp.ld, rows, ncol, 1, r0);
+        const Opnd A{xp.p + (long long)r0 * xp.ld, xp.ld, rows, xp.vec};
+        const Opnd B{xp.p, xp.ld, ncol, xp.vec};
+        tile_mma<Cfg32, true>(acc, A, B, w, ncol, smem);
+        acc_store<Cfg32>(acc, tp.p + (long long)r0 * tp.ld, tp.ld, rows, ncol, 1, r0, 0, 1.0);
+      }
+      __syncthreads();
+      if (tid == 0) {
+        __threadfence();
+        atomicAdd(counter(g, ws.ctr, tk.R, tk.q, tk.R), 1);
+      }
+    }
+    if (ws.prof != nullptr && tid == 0) {
+      const unsigned long long t2 = gtimer();
+      atomicAdd(ws.prof + 3 * tk.type, 1ull);
+      atomicAdd(ws.prof + 3 * tk.type + 1, t1 - t0);
+      atomicAdd(ws.prof + 3 * tk.type + 2, t2 - t1);
+    }
+    __syncthreads();
+  }
+}
+
+// out[0] = 2 * sum(slots[0:count]) in a fixed order (deterministic).
+__global__ void dag_logdet_kernel(const double* slots, int count, double* out) {
+  __shared__ double part[256];
+  const int tid = threadIdx.x;
+  const int per = (count + 255) / 256;
+  double acc = 0.0;
+  for (int i = tid * per; i < min(count, (tid + 1) * per); ++i) acc += slots[i];
+  part[tid] = acc;
+  __syncthreads();
+  for (int k = 128; k > 0; k >>= 1) {
+    if (tid < k) part[tid] += part[tid + k];
+    __syncthreads();
+  }
+  if (tid == 0) out[0] = 2.0 * part[0];
+}
 
 static size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 
-struct PobtafWs {
-  double* winv;
-  double* slots;
-  int nslots;
-};
+static Band make_band(double* data, int n, int b, int a, int use_arrow) {
+  Band g{};
+  g.data = data;
+  g.n = n; g.b = b; g.a = a;
+  g.nbt = (b + TT - 1) / TT;
+  g.nat = a > 0 ? (a + TT - 1) / TT : 0;
+  g.S = n * g.nbt + g.nat;
+  g.use_arrow = use_arrow && a > 0;
+  const bool base16 = ((uintptr_t)data % 16) == 0;
+  g.vec_b = base16 && (b % 2 == 0);
+  g.vec_a = g.vec_b && (a % 2 == 0);
+  return g;
+}
 
-static size_t pobtaf_ws(int n, int b, int a, char* base, PobtafWs* out) {
-  const int nl = leaves_of(b > a ? b : a);
-  const int nslots = n * leaves_of(b) + (a > 0 ? leaves_of(a) : 0);
-  size_t off = 0;
-  const size_t w = align_up((size_t)nl * LEAF * LEAF * sizeof(double));
-  const size_t s = align_up((size_t)(nslots > 0 ? nslots : 1) * sizeof(double));
-  if (out) {
-    out->winv = reinterpret_cast<double*>(base + off);
-    out->slots = reinterpret_cast<double*>(base + off + w);
-    out->nslots = nslots;
+// workspace: gstart | ctr, ticket, abort (one memset) | slots | W
+static size_t dag_ws(const Band& g, char* base, DagWs* o, size_t* zero_bytes) {
+  const int G = n_groups(g.S);
+  const size_t gs = align_up((size_t)(G + 1) * sizeof(int));
+  const long long nctr = counter_elems(g.n, g.nbt, g.nat, g.S);
+  const size_t cz = align_up((size_t)(nctr + 3) * sizeof(int));
+  const size_t sl = align_up((size_t)g.S * sizeof(double));
+  const size_t wb = (size_t)g.S * W_SLOT * sizeof(double);
+  if (o) {
+    o->gstart = reinterpret_cast<int*>(base);
+    o->ctr = reinterpret_cast<int*>(base + gs);
+    o->ticket = o->ctr + nctr;
+    o->abort_flag = o->ticket + 1;
+    o->role = o->ticket + 2;
+    o->slots = reinterpret_cast<double*>(base + gs + cz);
+    o->W = reinterpret_cast<double*>(base + gs + cz + sl);
+    o->G = G;
+    o->prof = nullptr;
   }
-  off += w + s;
-  return off;
+  if (zero_bytes) *zero_bytes = cz;
+  return gs + cz + sl + wb;
+}
+
+static int sm_count() {
+  int dev = 0, v = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+  return v > 0 ? v : 148;
 }
 
 }  // namespace stbta
@@ -64,7 +487,7 @@ using namespace stbta;
 
 extern "C" {
 
-const char* stbta_version(void) { return "stbta 0.1.0 (sm_100a, FP64 DMMA)"; }
+const char* stbta_version(void) { return "stbta 0.2.0 (sm_100a, FP64 DMMA task-graph)"; }
 
 long long stbta_storage_elems(int n, int b, int a) {
   return (long long)n * b * b + (long long)(n - 1) * b * b + (long long)n * a * b +
@@ -73,90 +496,62 @@ long long stbta_storage_elems(int n, int b, int a) {
 
 size_t stbta_pobtaf_workspace_bytes(int n, int b, int a) {
   if (n < 1 || b < 1 || a < 0) return 0;
-  return pobtaf_ws(n, b, a, nullptr, nullptr);
+  const Band g = make_band(nullptr, n, b, a, 1);
+  return dag_ws(g, nullptr, nullptr, nullptr);
 }
+
+static unsigned long long* g_prof = nullptr;  // debugging hook (stbta_debug_set_profile)
 
 int stbta_pobtaf(double* data, int n, int b, int a, int use_arrow, double* logdet_out, int* info,
                  void* workspace, size_t workspace_bytes, void* stream) {
   if (data == nullptr || n < 1 || b < 1 || a < 0 || info == nullptr) return STBTA_EARG;
   if (workspace_bytes < stbta_pobtaf_workspace_bytes(n, b, a)) return STBTA_EWORKSPACE;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  PobtafWs ws;
-  pobtaf_ws(n, b, a, reinterpret_cast<char*>(workspace), &ws);
-  BtaView m(data, n, b, a);
-  const bool arrow = use_arrow && a > 0;
-  const int lb = leaves_of(b);
-
+  const Band g = make_band(data, n, b, a, use_arrow);
+  DagWs ws;
+  size_t zbytes = 0;
+  dag_ws(g, reinterpret_cast<char*>(workspace), &ws, &zbytes);
+  ws.prof = g_prof;
+  static bool attr_done = false;  // idempotent attribute write
+  if (!attr_done) {
+    int e = (int)cudaFuncSetAttribute(pobtaf_dag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)DAG_SMEM_BYTES);
+    if (e) return e;
+    attr_done = true;
+  }
   int e = (int)cudaMemsetAsync(info, 0, sizeof(int), st);
   if (e) return e;
-  DenseCtx c{st, info, ws.winv, ws.slots};
-
-  for (int i = 0; i < n; ++i) {
-    e = potrf_rec(c, m.D(i), b, b, 0, i * lb, i + 1);
-    if (e) return e;
-    e = launch_zero_upper(m.D(i), b, b, info, st);
-    if (e) return e;
-    // panel S_i = [lower[i]; arrow[i]]  :=  S_i L_ii^-T
-    SegMat S;
-    int rows = 0;
-    if (i < n - 1) {
-      S = arrow ? seg2(m.Lo(i), b, b, m.Ar(i), b) : seg1(m.Lo(i), b);
-      rows = b + (arrow ? a : 0);
-    } else if (arrow) {
-      S = seg1(m.Ar(i), b);
-      rows = a;
-    }
-    if (rows == 0) continue;
-    e = trsm_rlt_rec(c, S, rows, m.D(i), b, b, 0);
-    if (e) return e;
-    // Schur update of [diag[i+1]; arrow[i+1] | tip] by S_i S_i^T (lower part)
-    GemmArgs g{};
-    g.A = S;
-    g.B = S;
-    g.M = rows;
-    g.N = rows;
-    g.K = b;
-    g.alpha = -1.0;
-    g.beta = 1.0;
-    g.c_lower = 1;
-    g.info = info;
-    g.batch = 1;
-    if (i < n - 1) {
-      g.C = seg2(m.D(i + 1), b, b, m.Ar(i + 1), b);
-      g.C.p2 = m.tip;
-      g.C.ld2 = a;
-      g.C.c0 = b;
-    } else {
-      g.C = seg1(m.tip, a);
-    }
-    e = gemm_launch(g, false, true, st);
-    if (e) return e;
-  }
-  if (a > 0) {
-    e = potrf_rec(c, m.tip, a, a, 0, n * lb, n + 1);
-    if (e) return e;
-    e = launch_zero_upper(m.tip, a, a, info, st);
-    if (e) return e;
-  }
+  if ((e = (int)cudaMemsetAsync(ws.ctr, 0, zbytes, st))) return e;
+  dag_setup_kernel<<<1, 1024, 0, st>>>(g, ws);
+  count_launch();
+  if ((e = (int)cudaGetLastError())) return e;
+  pobtaf_dag_kernel<<<sm_count(), DAG_NT, DAG_SMEM_BYTES, st>>>(g, ws, info);
+  count_launch();
+  if ((e = (int)cudaGetLastError())) return e;
   if (logdet_out != nullptr) {
-    e = launch_logdet_reduce(ws.slots, ws.nslots, logdet_out, st);
-    if (e) return e;
+    dag_logdet_kernel<<<1, 256, 0, st>>>(ws.slots, g.S, logdet_out);
+    count_launch();
+    if ((e = (int)cudaGetLastError())) return e;
   }
   return 0;
 }
+
+// Debug hook: a device buffer of 12 u64 that POBTAF accumulates per-task-type
+// {count, wait ns, exec ns} into (nullptr disables).  Not part of the stable ABI.
+void stbta_debug_set_profile(unsigned long long* buf) { g_prof = buf; }
 
 int stbta_dgemm(int ta, int tb, int M, int N, int K, double alpha, const double* A, long long lda,
                 const double* B, long long ldb, double beta, double* C, long long ldc,
                 void* stream) {
   if (M < 0 || N < 0 || K < 0) return STBTA_EARG;
-  GemmArgs g{};
-  g.A = seg1(const_cast<double*>(A), lda);
-  g.B = seg1(const_cast<double*>(B), ldb);
-  g.C = seg1(C, ldc);
-  g.M = M; g.N = N; g.K = K;
-  g.alpha = alpha; g.beta = beta;
-  g.batch = 1;
-  return gemm_launch(g, ta != 0, tb != 0, reinterpret_cast<cudaStream_t>(stream));
+  GemmArgs gm{};
+  gm.A = seg1(const_cast<double*>(A), lda);
+  gm.B = seg1(const_cast<double*>(B), ldb);
+  gm.C = seg1(C, ldc);
+  gm.M = M; gm.N = N; gm.K = K;
+  gm.alpha = alpha; gm.beta = beta;
+  gm.batch = 1;
+  return gemm_launch(gm, ta != 0, tb != 0, reinterpret_cast<cudaStream_t>(stream));
 }
 
 }  // extern "C"
