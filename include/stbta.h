@@ -118,15 +118,18 @@ long long stbta_launch_count(void);
  * NULL disables (the default). */
 void stbta_debug_set_profile(unsigned long long* buf);
 /* Debug micro-benchmark: `grid` CTAs each run `reps` tile products
- * C_t -= A_t B_t^T (128x128, K=128) of CTA shape `variant`. */
+ * C_t -= A_t B_t^T (128x128, depth K) of CTA shape `variant`. */
 int stbta_debug_tile_bench(int variant, const double* A, const double* B, double* C, int ntile,
-                           int reps, int grid, void* stream);
+                           int reps, int grid, int K, void* stream);
 /* Debug micro-benchmark: `grid` CTAs each factorize + invert the SPD 128x128
  * tile A `reps` times; ph (6 u64) receives CTA 0's phase times in ns. */
 int stbta_debug_potrf_bench(const double* A, double* out, int reps, int grid,
                             unsigned long long* ph, void* stream);
 /* Debug: clock cycles of `iters` dependent DMMA (which=0) or DFMA (1) on one warp. */
 int stbta_debug_latency(int which, int iters, double* scratch, long long* cycles, void* stream);
+/* Debug: DMMA throughput with shared-memory fragment loads (mode 0 LDS.64,
+ * 1 LDS.128, 2 none); FLOPs = grid*8*iters*8*32*512. */
+int stbta_debug_lds_bench(int mode, int iters, int grid, double* out, void* stream);
 int stbta_probe_dmma(int blocks, int iters, double* scratch, void* stream);
 int stbta_probe_dfma(int blocks, int iters, double* scratch, void* stream);
 

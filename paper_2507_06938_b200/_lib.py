@@ -44,8 +44,9 @@ _SIGNATURES = {
     "stbta_launch_count": (c_ll, []),
     "stbta_debug_set_profile": (None, [c_vp]),
     "stbta_debug_potrf_bench": (c_int, [c_vp, c_vp, c_int, c_int, c_vp, c_vp]),
+    "stbta_debug_lds_bench": (c_int, [c_int, c_int, c_int, c_vp, c_vp]),
     "stbta_debug_latency": (c_int, [c_int, c_int, c_vp, c_vp, c_vp]),
-    "stbta_debug_tile_bench": (c_int, [c_int, c_vp, c_vp, c_vp, c_int, c_int, c_int, c_vp]),
+    "stbta_debug_tile_bench": (c_int, [c_int, c_vp, c_vp, c_vp, c_int, c_int, c_int, c_int, c_vp]),
     "stbta_probe_dmma": (c_int, [c_int, c_int, c_vp, c_vp]),
     "stbta_probe_dfma": (c_int, [c_int, c_int, c_vp, c_vp]),
     "stbta_assemble_tile_elems": (c_int, []),

@@ -16,6 +16,8 @@ namespace stbta {
 // Host-side count of kernel launches issued by the library (bench.py's
 // gpu_launches; read with stbta_launch_count()).
 void count_launch();
+// Debug profile buffer set by stbta_debug_set_profile (nullptr: disabled).
+unsigned long long* debug_profile();
 
 // ---------------------------------------------------------------- cp.async
 // 8-byte element copy global->shared with zero fill when !valid.

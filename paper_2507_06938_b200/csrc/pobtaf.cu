@@ -500,7 +500,6 @@ size_t stbta_pobtaf_workspace_bytes(int n, int b, int a) {
   return dag_ws(g, nullptr, nullptr, nullptr);
 }
 
-static unsigned long long* g_prof = nullptr;  // debugging hook (stbta_debug_set_profile)
 
 int stbta_pobtaf(double* data, int n, int b, int a, int use_arrow, double* logdet_out, int* info,
                  void* workspace, size_t workspace_bytes, void* stream) {
@@ -511,7 +510,7 @@ int stbta_pobtaf(double* data, int n, int b, int a, int use_arrow, double* logde
   DagWs ws;
   size_t zbytes = 0;
   dag_ws(g, reinterpret_cast<char*>(workspace), &ws, &zbytes);
-  ws.prof = g_prof;
+  ws.prof = debug_profile();
   static bool attr_done = false;  // idempotent attribute write
   if (!attr_done) {
     int e = (int)cudaFuncSetAttribute(pobtaf_dag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -535,10 +534,6 @@ int stbta_pobtaf(double* data, int n, int b, int a, int use_arrow, double* logde
   }
   return 0;
 }
-
-// Debug hook: a device buffer of 12 u64 that POBTAF accumulates per-task-type
-// {count, wait ns, exec ns} into (nullptr disables).  Not part of the stable ABI.
-void stbta_debug_set_profile(unsigned long long* buf) { g_prof = buf; }
 
 int stbta_dgemm(int ta, int tb, int M, int N, int K, double alpha, const double* A, long long lda,
                 const double* B, long long ldb, double beta, double* C, long long ldc,

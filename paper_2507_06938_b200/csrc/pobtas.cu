@@ -3,402 +3,517 @@
 // Reference: bta.forward_substitute (pkg/src/stinla/bta.py:249-275),
 // bta.backward_substitute (bta.py:278-302), bta.solve (bta.py:305-307).
 //
-// B200 mapping.  The block-bidiagonal part of L (diag + lower blocks) is a
-// banded lower-triangular matrix; each sweep is ONE persistent-style launch
-// over 64-row chunks.  A chunk takes a ticket from an atomic counter (so a
-// chunk only ever waits on chunks that are already running: no deadlock),
-// streams its row band of L from HBM (prefetched into registers before it waits
-// on the producer flag of the matching solution chunk), then solves its 64x64
-// diagonal tile in a warp.  The only sequential part is that 64x64 tile and a
-// flag hand-off; everything else streams the factor at HBM rate.  The arrow
-// rows / tip (a <= 64) are a fixed-order reduction plus an a x a solve.
+// B200 mapping.  The block-bidiagonal part of L is a banded lower-triangular
+// matrix cut into 128-row tiles (band.cuh geometry).  Each sweep is ONE
+// launch in which a CTA takes tile R from an atomic ticket (so it only ever
+// waits on tiles already claimed) and
+//   1. streams the matrix blocks coupling R to its dependencies (tiles of the
+//      previous / next time block and of its own block) through a 4-stage
+//      cp.async ring of 32-column (32-row) slices -- the factor is read
+//      exactly once per sweep at HBM rate, prefetched before the dependency's
+//      solution is even ready;
+//   2. folds each dependency's solution in, in a fixed order (deterministic),
+//      as soon as that tile publishes it (acquire flag);
+//   3. solves its 128x128 diagonal triangle in 32-row blocks (warp-level
+//      substitution + block updates) and publishes the tile (release flag).
+// The arrow rows become per-tile partial products summed in tile order by the
+// tip kernel, which also solves L_tip (reference bta.py:263-273, 288-300).
 #include "../../include/stbta.h"
+#include "band.cuh"
 #include "common.cuh"
-#include "stbta_internal.cuh"
+#include "potrf_tile.cuh"
 
 namespace stbta {
 
-constexpr int CH = 64;     // chunk rows (== LEAF)
-constexpr int NRMAX = 8;   // right-hand sides per sweep launch
+constexpr int PS_NT = 256;
+constexpr int NR = 8;      // right-hand sides per sweep launch
+constexpr int SL = 32;     // slice width
+constexpr int PST = 3;     // ring stages
+constexpr int F_LD = SL + 1;           // forward slice: 128 rows x 32 cols
+constexpr int B_LD = 128 + 1;          // backward slice: 32 rows x 128 cols
+constexpr int STAGE = 128 * F_LD > SL * B_LD ? 128 * F_LD : SL * B_LD;
+constexpr int P_LD = 129;              // coupling block in shared memory
+constexpr int WPK = 128 * 129 / 2;     // packed lower 128 x 128
+constexpr int PS_SMEM_DOUBLES = WPK + 128 * P_LD + 128 * NR + 128 * NR;
+static_assert(PST * STAGE <= 128 * P_LD, "ring must fit in the coupling-block region");
+
+STBTA_DEV int pk(int r, int c) { return r * (r + 1) / 2 + c; }
 
 struct SweepArgs {
-  const double* diag;
-  const double* lower;
-  const double* arrow;
-  const double* tip;
-  int n, b, a, nck, has_arrow;
-  double* x;          // rhs / solution, row-major (dim x ldx), columns [0, ncols)
+  Band g;
+  double* x;      // rhs / solution, row-major (dim x ldx), columns [0, ncols)
   long long ldx;
   int ncols;
-  int* flags;         // one per chunk, zeroed before the launch
-  int* ticket;        // zeroed before the launch
+  int ntile;      // n * nbt block tiles
+  int* flags;     // one per tile, zeroed before the launch
+  int* ticket;    // zeroed before the launch
+  double* part;   // arrow partials [ntile][a][NR] (forward)
+  const double* xtip;  // packed x_tip [a][NR] (backward)
+  double* push;   // [ntile][128][NR]: coupling contribution pushed to the next tile
+  unsigned long long* prof;  // optional debug timers (slots 20..23)
+  const double* winv;  // [ntile][WPK]: packed inverses of the diagonal tiles
 };
 
-STBTA_DEV int acquire_ld(const int* p) {
-  int v;
-  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
-  return v;
+// ---------------------------------------------------------------- pre-pass
+// W_R = L_RR^-1 for every diagonal tile, packed lower (row-major).  Blocked:
+// warp kb inverts the 32x32 diagonal block kb (one column per lane), then the
+// off-diagonal blocks by diagonals, W_ij = -W_ii sum_{k=j}^{i-1} L_ik W_kj.
+constexpr int INV_LD = 129, BLD = 33;
+constexpr int INV_SMEM_DOUBLES = 128 * INV_LD + 11 * 32 * BLD;
+
+__global__ void __launch_bounds__(PS_NT, 1) inv_tiles_kernel(Band g, double* winv) {
+  extern __shared__ __align__(16) double sm[];
+  double* T = sm;                       // L lower; W_ij^T (i > j) in upper block (j, i)
+  double* WT = T + 128 * INV_LD;        // W_kk^T: WT[kb][c][i] = W_kk[i][c]
+  double* Wd = WT + 4 * 32 * BLD;       // W_kk row-major
+  double* TS = Wd + 4 * 32 * BLD;       // scratch products, 3 blocks
+  const int R = blockIdx.x;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int ext = tile_extent(g, R);
+  const TilePtr tp = tile_ptr(g, R, R);
+  for (int e = tid; e < 128 * 128; e += PS_NT) {
+    const int r = e >> 7, c = e & 127;
+    double v;
+    if (r < ext && c < ext) v = (c <= r) ? __ldg(tp.p + (long long)r * tp.ld + c) : 0.0;
+    else v = (r == c) ? 1.0 : 0.0;
+    T[r * INV_LD + c] = v;
+  }
+  __syncthreads();
+  if (warp < 4) {
+    const int k0 = warp * 32;
+    double* dinv = TS + warp * 32;
+    dinv[lane] = 1.0 / T[(k0 + lane) * INV_LD + k0 + lane];
+    __syncwarp();
+    double w[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) w[i] = (i == lane) ? 1.0 : 0.0;
+#pragma unroll 32
+    for (int k = 0; k < 32; ++k) {
+      w[k] *= dinv[k];
+#pragma unroll 32
+      for (int i = k + 1; i < 32; ++i) w[i] = fma(-T[(k0 + i) * INV_LD + k0 + k], w[k], w[i]);
+    }
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      WT[warp * 32 * BLD + lane * BLD + i] = w[i];
+      Wd[warp * 32 * BLD + i * BLD + lane] = w[i];
+    }
+  }
+  __syncthreads();
+  for (int d = 1; d < 4; ++d) {
+    const int nb = 4 - d, blk = tid >> 6, id = tid & 63, tr = id & 7, tc = id >> 3;
+    if (blk < nb) {  // T_j = sum_k L_ik W_kj  (i = j + d)
+      const int j = blk, i = j + d;
+      double acc[4][4];
+      zero4x4(acc);
+      for (int k = j; k < i; ++k) {
+        const double* b = (k == j) ? WT + j * 32 * BLD : T + (32 * j) * INV_LD + 32 * k;
+        const int ldb = (k == j) ? BLD : INV_LD;
+        mma32_blk<32, true>(acc, T + (32 * i) * INV_LD + 32 * k, INV_LD, b, ldb, id);
+      }
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) TS[j * 32 * BLD + (tr + 8 * a) * BLD + tc + 8 * c] = acc[a][c];
+    }
+    __syncthreads();
+    if (blk < nb) {  // W_ij = -W_ii T_j, stored transposed into T's upper block (j, i)
+      const int j = blk, i = j + d;
+      double acc[4][4];
+      zero4x4(acc);
+      mma32_blk<32, false>(acc, Wd + i * 32 * BLD, BLD, TS + j * 32 * BLD, BLD, id);
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          T[(32 * j + tc + 8 * c) * INV_LD + 32 * i + tr + 8 * a] = -acc[a][c];
+    }
+    __syncthreads();
+  }
+  double* out = winv + (long long)R * WPK;
+  for (int e = tid; e < WPK; e += PS_NT) {
+    int r = (int)((sqrtf(8.0f * e + 1.0f) - 1.0f) * 0.5f);
+    if ((r + 1) * (r + 2) / 2 <= e) ++r;
+    if (r * (r + 1) / 2 > e) --r;
+    const int c = e - r * (r + 1) / 2;
+    double v;
+    if ((r >> 5) == (c >> 5)) v = Wd[(r >> 5) * 32 * BLD + (r & 31) * BLD + (c & 31)];
+    else v = T[c * INV_LD + r];
+    out[e] = v;
+  }
 }
-STBTA_DEV void release_st(int* p, int v) {
-  asm volatile("st.release.gpu.global.s32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+
+// One 32-wide slice of dependency tile k into a ring stage.
+template <bool FWD>
+STBTA_DEV void load_slice(double* ring_st, const Band& g, int R, int k, int sl, int extR,
+                          int extK) {
+  const int tid = threadIdx.x;
+  if (FWD) {
+    // M = tile (R, k): rows r < extR, cols sl*32 + q (q < 32, < extK)
+    const TilePtr t = tile_ptr(g, R, k);
+    const int c0 = sl * SL;
+    for (int e = tid; e < 128 * SL; e += PS_NT) {
+      const int r = e >> 5, q = e & 31;
+      if (r < extR && c0 + q < extK)
+        cp_async8(ring_st + r * F_LD + q, t.p + (long long)r * t.ld + c0 + q, true);
+      else
+        ring_st[r * F_LD + q] = 0.0;
+    }
+  } else {
+    // M = tile (k, R): rows sl*32 + q of tile k (q < 32, < extK), cols r < extR
+    const TilePtr t = tile_ptr(g, k, R);
+    const int r0 = sl * SL;
+    for (int e = tid; e < SL * 128; e += PS_NT) {
+      const int q = e >> 7, r = e & 127;
+      if (r0 + q < extK && r < extR)
+        cp_async8(ring_st + q * B_LD + r, t.p + (long long)(r0 + q) * t.ld + r, true);
+      else
+        ring_st[q * B_LD + r] = 0.0;
+    }
+  }
 }
-STBTA_DEV void wait_flag(const int* f) {
-  if (threadIdx.x == 0) {
-    while (acquire_ld(f) == 0) __nanosleep(64);
+
+// out[r] (r < 128, c < NR) = sum_q M(r, q) v[q], M given by an accessor; the
+// 256 threads split q in halves, partial sums combined in a fixed order.
+template <int NRC, class F>
+STBTA_DEV void gemv128(double* out, const double* v, double* tmp, F M) {
+  const int tid = threadIdx.x, r = tid & 127, h = tid >> 7;
+  double s[NRC];
+#pragma unroll
+  for (int c = 0; c < NRC; ++c) s[c] = 0.0;
+#pragma unroll 4
+  for (int qq = 0; qq < 64; ++qq) {
+    const int q = h * 64 + qq;
+    const double m = M(r, q);
+#pragma unroll
+    for (int c = 0; c < NRC; ++c) s[c] = fma(m, v[q * NR + c], s[c]);
+  }
+  if (h == 1) {
+#pragma unroll
+    for (int c = 0; c < NRC; ++c) tmp[r * NR + c] = s[c];
+  }
+  __syncthreads();
+  if (h == 0) {
+#pragma unroll
+    for (int c = 0; c < NRC; ++c) out[r * NR + c] = s[c] + tmp[r * NR + c];
   }
   __syncthreads();
 }
 
-// ------------------------------------------------------------ forward sweep
-// chunk (i, j): rows ib + 64j + [0, rows).  y_R = L_RR^-1 (r_R - sum_deps L_R,D y_D)
-__global__ void __launch_bounds__(256) fwd_sweep_kernel(SweepArgs p) {
+template <bool FWD, int NRC>
+__global__ void __launch_bounds__(PS_NT, 1) sweep_kernel(SweepArgs p) {
+  extern __shared__ __align__(16) double sm[];
+  double* Wp = sm;                   // packed W of this tile
+  double* Pb = Wp + WPK;             // ring for the pulled dependencies, then the push block
+  double* ybuf = Pb + 128 * P_LD;    // dependency solution / this tile's solution, 128 x NR
+  double* accb = ybuf + 128 * NR;    // right-hand side, 128 x NR
+  double* ring = Pb;
   __shared__ int s_k;
-  __shared__ double ys[CH][NRMAX];
-  __shared__ double Ls[CH][CH + 1];
-  __shared__ double accs[CH][NRMAX];
-  const int tid = threadIdx.x;
+  const Band& g = p.g;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) s_k = atomicAdd(p.ticket, 1);
   __syncthreads();
-  const int k = s_k;
-  const int i = k / p.nck, j = k % p.nck;
-  const int b = p.b;
-  const int rows = min(CH, b - j * CH);
-  const long long grow0 = (long long)i * b + (long long)j * CH;
-  const int rr = tid >> 2, q = tid & 3;
+  const int R = FWD ? s_k : p.ntile - 1 - s_k;
+  const int i = R / g.nbt;
+  const int extR = tile_extent(g, R);
+  const long long row0 = (long long)i * g.b + (long long)(R % g.nbt) * 128;
   const int nc = p.ncols;
+  unsigned long long t0 = 0, t1 = 0, t2 = 0;
+  if (p.prof && tid == 0) t0 = pt_timer();
 
-  double acc[NRMAX];
-#pragma unroll
-  for (int r = 0; r < NRMAX; ++r) acc[r] = 0.0;
+  // packed inverse of the diagonal tile (own cp.async group, waited on late)
+  {
+    const double* src = p.winv + (long long)R * WPK;
+    for (int e = tid; e < WPK / 2; e += PS_NT) cp_async16(Wp + 2 * e, src + 2 * e, 16);
+    cp_async_commit();
+  }
 
-  // dependency list: all chunks of block i-1 (through lower[i-1]), then chunks
-  // 0..j-1 of block i (through diag[i])
-  const int ndep = (i > 0 ? p.nck : 0) + j;
-  for (int d = 0; d < ndep; ++d) {
-    int bi, bj;
-    const double* M;
-    if (i > 0 && d < p.nck) {
-      bi = i - 1; bj = d; M = p.lower + (long long)(i - 1) * b * b;
-    } else {
-      bi = i; bj = d - (i > 0 ? p.nck : 0); M = p.diag + (long long)i * b * b;
-    }
-    const int c0 = bj * CH;
-    const int dcols = min(CH, b - c0);
-    // prefetch this thread's 16 entries of the L row band before waiting
-    double lv[16];
-    const bool row_ok = rr < rows;
-    const double* mrow = M + (long long)(j * CH + rr) * b + c0 + q * 16;
-#pragma unroll
-    for (int t = 0; t < 16; ++t) {
-      const int col = q * 16 + t;
-      lv[t] = (row_ok && col < dcols) ? __ldg(mrow + t) : 0.0;
-    }
-    wait_flag(p.flags + bi * p.nck + bj);
-    const long long drow0 = (long long)bi * b + c0;
-    for (int e = tid; e < CH * NRMAX; e += 256) {
-      const int t = e / NRMAX, r = e % NRMAX;
-      ys[t][r] = (t < dcols && r < nc) ? __ldcg(p.x + (drow0 + t) * p.ldx + r) : 0.0;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int t = 0; t < 16; ++t) {
-#pragma unroll
-      for (int r = 0; r < NRMAX; ++r) acc[r] -= lv[t] * ys[q * 16 + t][r];
-    }
-    __syncthreads();
+  // pulled dependencies: forward k in [lo, R-1) ascending; backward k in (R+1, hi] descending
+  // (the adjacent tile is pushed: it sends its coupling product with its flag)
+  int kfirst, nk, crit;
+  if (FWD) {
+    const int lo = max(0, (i - 1) * g.nbt);
+    kfirst = lo;
+    nk = max(0, R - 1 - lo);
+    crit = R - 1;  // -1 for the first tile
+  } else {
+    const int hi = min((i + 2) * g.nbt, p.ntile) - 1;
+    kfirst = hi;
+    nk = max(0, hi - R - 1);
+    crit = (R + 1 < p.ntile) ? R + 1 : -1;
   }
-#pragma unroll
-  for (int r = 0; r < NRMAX; ++r) {
-    acc[r] += __shfl_xor_sync(0xffffffffu, acc[r], 1);
-    acc[r] += __shfl_xor_sync(0xffffffffu, acc[r], 2);
-  }
-  if (q == 0) {
-#pragma unroll
-    for (int r = 0; r < NRMAX; ++r)
-      accs[rr][r] = (rr < rows && r < nc) ? __ldcg(p.x + (grow0 + rr) * p.ldx + r) + acc[r] : 0.0;
-  }
-  const double* Dt = p.diag + (long long)i * b * b + (long long)(j * CH) * b + j * CH;
-  for (int e = tid; e < CH * CH; e += 256) {
-    const int r = e / CH, c = e % CH;
-    Ls[r][c] = (r < rows && c <= r) ? Dt[(long long)r * b + c] : 0.0;
-  }
-  __syncthreads();
-  if (tid < 32) {  // warp substitution, lanes own rows lane and lane+32
-    const int l = tid;
-    double v0[NRMAX], v1[NRMAX];
-#pragma unroll
-    for (int r = 0; r < NRMAX; ++r) { v0[r] = accs[l][r]; v1[r] = accs[l + 32][r]; }
-    for (int t = 0; t < rows; ++t) {
-      const double inv = 1.0 / Ls[t][t];
-      const double m0 = Ls[l][t], m1 = Ls[l + 32][t];
-#pragma unroll
-      for (int r = 0; r < NRMAX; ++r) {
-        const double own = (t < 32) ? v0[r] : v1[r];
-        const double yt = __shfl_sync(0xffffffffu, own, t & 31) * inv;
-        if (l == (t & 31)) { if (t < 32) v0[r] = yt; else v1[r] = yt; }
-        if (l > t) v0[r] -= m0 * yt;
-        if (l + 32 > t) v1[r] -= m1 * yt;
-      }
-    }
-#pragma unroll
-    for (int r = 0; r < NRMAX; ++r) {
-      if (r < nc) {
-        if (l < rows) p.x[(grow0 + l) * p.ldx + r] = v0[r];
-        if (l + 32 < rows) p.x[(grow0 + l + 32) * p.ldx + r] = v1[r];
-      }
-    }
-    __syncwarp();
-    if (tid == 0) {
-      __threadfence();
-      release_st(p.flags + k, 1);
-    }
-  }
-}
+  auto dep = [&](int d) { return FWD ? kfirst + d : kfirst - d; };
+  auto nsl = [&](int k) { return (tile_extent(g, k) + SL - 1) / SL; };
 
-// ----------------------------------------------------------- backward sweep
-// chunk (i, j) in reverse order: x_R = L_RR^-T (y_R - sum L_D,R^T x_D - A_R^T x_tip)
-__global__ void __launch_bounds__(256) bwd_sweep_kernel(SweepArgs p, const double* xtip) {
-  __shared__ int s_k;
-  __shared__ double xs[CH][NRMAX];
-  __shared__ double big[CH * (CH + 1)];  // partial sums first, then the diagonal tile
-  double(*Ls)[CH + 1] = reinterpret_cast<double(*)[CH + 1]>(big);
-  double(*part)[CH][NRMAX] = reinterpret_cast<double(*)[CH][NRMAX]>(big);
-  const int tid = threadIdx.x;
-  const int total = p.n * p.nck;
-  if (tid == 0) s_k = total - 1 - atomicAdd(p.ticket, 1);
-  __syncthreads();
-  const int k = s_k;
-  const int i = k / p.nck, j = k % p.nck;
-  const int b = p.b;
-  const int cols = min(CH, b - j * CH);  // rows of this chunk == columns of L used
-  const long long grow0 = (long long)i * b + (long long)j * CH;
-  const int c = tid & 63, rq = tid >> 6;
-  const int nc = p.ncols;
+  const int r = tid & 127, h = tid >> 7;
+  double acc[NRC];
+#pragma unroll
+  for (int c = 0; c < NRC; ++c) acc[c] = 0.0;
 
-  double acc[NRMAX];
+  if (!FWD && g.use_arrow && h == 0 && r < extR) {  // x_R -= arrow[i][:, R]^T x_tip
+    const long long bb = (long long)g.b * g.b;
+    const double* arrow = g.data + (long long)(2 * g.n - 1) * bb + (long long)i * g.a * g.b;
+    const int col = (R % g.nbt) * 128 + r;
+    for (int t = 0; t < g.a; ++t) {
+      const double av = arrow[(long long)t * g.b + col];
 #pragma unroll
-  for (int r = 0; r < NRMAX; ++r) acc[r] = 0.0;
+      for (int c = 0; c < NRC; ++c)
+        if (c < nc) acc[c] -= av * p.xtip[t * NR + c];
+    }
+  }
 
-  // dependencies, earliest-finished first: chunks of block i+1 (through
-  // lower[i]) from the last one down, then chunks j+1.. of block i (diag[i])
-  const int nnext = (i + 1 < p.n) ? p.nck : 0;
-  const int nself = p.nck - 1 - j;
-  for (int d = 0; d < nnext + nself; ++d) {
-    int bi, bj;
-    const double* M;
-    if (d < nnext) {
-      bi = i + 1; bj = p.nck - 1 - d; M = p.lower + (long long)i * b * b;
-    } else {
-      bi = i; bj = p.nck - 1 - (d - nnext); M = p.diag + (long long)i * b * b;
+  int total = 0;
+  for (int d = 0; d < nk; ++d) total += nsl(dep(d));
+  int pd = 0, ps = 0;
+  auto issue = [&](int stage) {
+    if (pd < nk) {
+      const int k = dep(pd);
+      load_slice<FWD>(ring + stage * STAGE, g, R, k, ps, extR, tile_extent(g, k));
+      if (++ps == nsl(k)) { ps = 0; ++pd; }
     }
-    const int r0 = bj * CH;
-    const int drows = min(CH, b - r0);
-    double lv[16];
-#pragma unroll
-    for (int t = 0; t < 16; ++t) {
-      const int rloc = rq * 16 + t;
-      lv[t] = (c < cols && rloc < drows) ? __ldg(M + (long long)(r0 + rloc) * b + j * CH + c) : 0.0;
-    }
-    wait_flag(p.flags + bi * p.nck + bj);
-    const long long drow0 = (long long)bi * b + r0;
-    for (int e = tid; e < CH * NRMAX; e += 256) {
-      const int t = e / NRMAX, r = e % NRMAX;
-      xs[t][r] = (t < drows && r < nc) ? __ldcg(p.x + (drow0 + t) * p.ldx + r) : 0.0;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int t = 0; t < 16; ++t) {
-#pragma unroll
-      for (int r = 0; r < NRMAX; ++r) acc[r] -= lv[t] * xs[rq * 16 + t][r];
-    }
-    __syncthreads();
-  }
-  // arrow coupling: x_R -= arrow[i][:, R]^T x_tip  (bta.py:297-298)
-  if (p.has_arrow && rq == 0 && c < cols) {
-    const double* A = p.arrow + (long long)i * p.a * b + j * CH + c;
-    for (int t = 0; t < p.a; ++t) {
-      const double av = A[(long long)t * b];
-#pragma unroll
-      for (int r = 0; r < NRMAX; ++r)
-        if (r < nc) acc[r] -= av * xtip[t * NRMAX + r];
-    }
-  }
-#pragma unroll
-  for (int r = 0; r < NRMAX; ++r) part[rq][c][r] = acc[r];
-  __syncthreads();
-  double v0[NRMAX], v1[NRMAX];
-  const int l = tid & 31;
-  if (tid < 32) {
-#pragma unroll
-    for (int r = 0; r < NRMAX; ++r) {
-      const double y0 = (l < cols && r < nc) ? __ldcg(p.x + (grow0 + l) * p.ldx + r) : 0.0;
-      const double y1 = (l + 32 < cols && r < nc) ? __ldcg(p.x + (grow0 + l + 32) * p.ldx + r) : 0.0;
-      v0[r] = y0 + ((part[0][l][r] + part[1][l][r]) + (part[2][l][r] + part[3][l][r]));
-      v1[r] = y1 + ((part[0][l + 32][r] + part[1][l + 32][r]) +
-                    (part[2][l + 32][r] + part[3][l + 32][r]));
-    }
-  }
-  __syncthreads();
-  const double* Dt = p.diag + (long long)i * b * b + (long long)(j * CH) * b + j * CH;
-  for (int e = tid; e < CH * CH; e += 256) {
-    const int r = e / CH, cc = e % CH;
-    Ls[r][cc] = (r < cols && cc <= r) ? Dt[(long long)r * b + cc] : 0.0;
-  }
-  __syncthreads();
-  if (tid < 32) {
-    for (int t = cols - 1; t >= 0; --t) {
-      const double inv = 1.0 / Ls[t][t];
-      const double m0 = Ls[t][l], m1 = Ls[t][l + 32];  // (L^T)[l][t] = L[t][l]
-#pragma unroll
-      for (int r = 0; r < NRMAX; ++r) {
-        const double own = (t < 32) ? v0[r] : v1[r];
-        const double xt = __shfl_sync(0xffffffffu, own, t & 31) * inv;
-        if (l == (t & 31)) { if (t < 32) v0[r] = xt; else v1[r] = xt; }
-        if (l < t) v0[r] -= m0 * xt;
-        if (l + 32 < t) v1[r] -= m1 * xt;
-      }
-    }
-#pragma unroll
-    for (int r = 0; r < NRMAX; ++r) {
-      if (r < nc) {
-        if (l < cols) p.x[(grow0 + l) * p.ldx + r] = v0[r];
-        if (l + 32 < cols) p.x[(grow0 + l + 32) * p.ldx + r] = v1[r];
-      }
-    }
-    __syncwarp();
-    if (tid == 0) {
-      __threadfence();
-      release_st(p.flags + k, 1);
-    }
-  }
-}
+    cp_async_commit();
+  };
+  for (int s = 0; s < PST - 1; ++s) issue(s);
 
-// -------------------------------------------------------------- arrow / tip
-// partial[g][t][r] = sum over this CTA's columns of arrow[t][col] * y[col][r]
-__global__ void __launch_bounds__(256) arrow_partial_kernel(SweepArgs p, double* partial,
-                                                            int cols_per_cta) {
-  const int tid = threadIdx.x;
-  const long long N = (long long)p.n * p.b;
-  const long long c_beg = (long long)blockIdx.x * cols_per_cta;
-  const long long c_end = min(N, c_beg + cols_per_cta);
-  const int a = p.a, nc = p.ncols;
-  for (int t = 0; t < a; ++t) {
-    for (int r = 0; r < nc; ++r) {
-      double s = 0.0;
-      for (long long col = c_beg + tid; col < c_end; col += 256) {
-        const long long blk = col / p.b, cc = col % p.b;
-        s += p.arrow[(blk * a + t) * p.b + cc] * p.x[col * p.ldx + r];
-      }
-      s = warp_sum(s);
-      __shared__ double wsum[8];
-      if ((tid & 31) == 0) wsum[tid >> 5] = s;
+  int cd = 0, cs = 0;
+  for (int it = 0; it < total; ++it) {
+    const int k = dep(cd);
+    if (cs == 0) {
       __syncthreads();
       if (tid == 0) {
-        double tot = 0.0;
-        for (int w = 0; w < 8; ++w) tot += wsum[w];
-        partial[((long long)blockIdx.x * a + t) * NRMAX + r] = tot;
+        while (ld_acquire(p.flags + k) == 0) __nanosleep(20);
       }
       __syncthreads();
+      const long long krow0 = (long long)(k / g.nbt) * g.b + (long long)(k % g.nbt) * 128;
+      const int extK = tile_extent(g, k);
+      for (int e = tid; e < 128 * NR; e += PS_NT) {
+        const int q = e / NR, c = e % NR;
+        ybuf[e] = (q < extK && c < nc) ? __ldcg(p.x + (krow0 + q) * p.ldx + c) : 0.0;
+      }
+    }
+    cp_async_wait<PST - 2>();
+    __syncthreads();
+    issue((it + PST - 1) % PST);
+    const double* rs = ring + (it % PST) * STAGE;
+    const int q0 = cs * SL;
+#pragma unroll 4
+    for (int qq = 0; qq < SL / 2; ++qq) {
+      const int q = h * (SL / 2) + qq;
+      const double m = FWD ? rs[r * F_LD + q] : rs[q * B_LD + r];
+      const double* yq = ybuf + (q0 + q) * NR;
+#pragma unroll
+      for (int c = 0; c < NRC; ++c) acc[c] = fma(-m, yq[c], acc[c]);
+    }
+    if (++cs == nsl(k)) { cs = 0; ++cd; }
+  }
+  cp_async_wait<0>();
+  __syncthreads();
+  if (p.prof && tid == 0) t1 = pt_timer();
+
+  // prefetch the push block: forward tile (R+1, R) [rows of R+1 x cols of R],
+  // backward tile (R, R-1) [rows of R x cols of R-1]
+  const int pushto = FWD ? ((R + 1 < p.ntile) ? R + 1 : -1) : R - 1;
+  if (pushto >= 0) {
+    const TilePtr t = FWD ? tile_ptr(g, R + 1, R) : tile_ptr(g, R, R - 1);
+    const int nr = FWD ? tile_extent(g, R + 1) : extR;
+    const int ncl = FWD ? extR : tile_extent(g, R - 1);
+    for (int e = tid; e < 128 * 128; e += PS_NT) {
+      const int rr = e >> 7, cc = e & 127;
+      if (rr < nr && cc < ncl) cp_async8(Pb + rr * P_LD + cc, t.p + (long long)rr * t.ld + cc, true);
+      else Pb[rr * P_LD + cc] = 0.0;
+    }
+  }
+  cp_async_commit();
+
+  // accb = rhs + pulled contributions (h0 then h1, fixed order)
+  if (h == 0) {
+#pragma unroll
+    for (int c = 0; c < NR; ++c)
+      accb[r * NR + c] = (c < NRC && r < extR && c < nc) ? __ldcg(p.x + (row0 + r) * p.ldx + c) + acc[c < NRC ? c : 0] : 0.0;
+  }
+  __syncthreads();
+  if (h == 1) {
+#pragma unroll
+    for (int c = 0; c < NRC; ++c) accb[r * NR + c] += (r < extR && c < nc) ? acc[c] : 0.0;
+  }
+  // the adjacent (critical) tile's pushed contribution
+  if (crit >= 0) {
+    if (tid == 0) {
+      while (ld_acquire(p.flags + crit) == 0) __nanosleep(10);
+    }
+    __syncthreads();
+    if (h == 0) {
+      const double* u = p.push + (long long)R * 128 * NR;
+#pragma unroll
+      for (int c = 0; c < NRC; ++c) accb[r * NR + c] -= (r < extR && c < nc) ? __ldcg(u + r * NR + c) : 0.0;
+    }
+  }
+  cp_async_wait<0>();
+  __syncthreads();
+  if (p.prof && tid == 0) t2 = pt_timer();
+  // y = W acc (forward)  /  x = W^T acc (backward); result in ybuf
+  if (FWD)
+    gemv128<NRC>(ybuf, accb, ybuf, [&](int rr, int q) { return q <= rr ? Wp[pk(rr, q)] : 0.0; });
+  else
+    gemv128<NRC>(ybuf, accb, ybuf, [&](int rr, int q) { return q >= rr ? Wp[pk(q, rr)] : 0.0; });
+  // push: forward u = L_{R+1,R} y  ->  push[R+1];  backward v = L_{R,R-1}^T x -> push[R-1]
+  if (pushto >= 0) {
+    if (FWD)
+      gemv128<NRC>(accb, ybuf, accb, [&](int rr, int q) { return Pb[rr * P_LD + q]; });
+    else
+      gemv128<NRC>(accb, ybuf, accb, [&](int rr, int q) { return Pb[q * P_LD + rr]; });
+    double* dst = p.push + (long long)pushto * 128 * NR;
+    for (int e = tid; e < 128 * NR; e += PS_NT) dst[e] = accb[e];
+  }
+  // publish the solution
+  for (int e = tid; e < extR * NR; e += PS_NT) {
+    const int rr = e / NR, c = e % NR;
+    if (c < nc) p.x[(row0 + rr) * p.ldx + c] = ybuf[e];
+  }
+  if (FWD && g.use_arrow) {  // arrow partials: part[R][t][c] = sum_r arrow[i][t][R0 + r] y[r][c]
+    const long long bb = (long long)g.b * g.b;
+    const double* arrow = g.data + (long long)(2 * g.n - 1) * bb + (long long)i * g.a * g.b;
+    const int col0 = (R % g.nbt) * 128;
+    for (int t = warp; t < g.a; t += PS_NT / 32) {
+      double s[NRC];
+#pragma unroll
+      for (int c = 0; c < NRC; ++c) s[c] = 0.0;
+      for (int rr = lane; rr < extR; rr += 32) {
+        const double av = arrow[(long long)t * g.b + col0 + rr];
+#pragma unroll
+        for (int c = 0; c < NRC; ++c) s[c] = fma(av, ybuf[rr * NR + c], s[c]);
+      }
+#pragma unroll
+      for (int c = 0; c < NRC; ++c) {
+        const double v = warp_sum(s[c]);
+        if (lane == 0) p.part[((long long)R * g.a + t) * NR + c] = v;
+      }
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    atomicExch(p.flags + R, 1);
+    if (p.prof) {
+      const unsigned long long t3 = pt_timer();
+      atomicAdd(p.prof + 20, 1ull);
+      atomicAdd(p.prof + 21, t1 - t0);
+      atomicAdd(p.prof + 22, t2 - t1);
+      atomicAdd(p.prof + 23, t3 - t2);
     }
   }
 }
 
-// mode 0 (forward): y_tip = L_tip^-1 (r_tip - sum_g partial[g]);  mode 1: x_tip = L_tip^-T y_tip.
-// Works in place on the tip segment of x (any arrow size) and writes a packed
-// copy xtip[a][NRMAX] for the backward sweep's arrow coupling.
-__global__ void tip_solve_kernel(SweepArgs p, const double* partial, int nparts, double* xtip,
-                                 int mode) {
-  const int r = threadIdx.x;
-  if (r >= p.ncols) return;
-  const int a = p.a;
-  const long long base = (long long)p.n * p.b;
-  double* v = p.x + base * p.ldx + r;  // v[t * ldx]
+// mode 0 (forward): y_tip = L_tip^-1 (r_tip - sum_R part[R]);  mode 1: x_tip = L_tip^-T y_tip.
+// In place on the tip segment of x (any arrow size); writes a packed copy
+// xtip[a][NR] for the backward sweep's arrow coupling.
+__global__ void tip_solve_kernel(SweepArgs p, int nparts, double* xtip, int mode) {
+  const int c = threadIdx.x;
+  if (c >= p.ncols) return;
+  const Band& g = p.g;
+  const int a = g.a;
+  const long long base = (long long)g.n * g.b;
+  const double* tip = g.data + (long long)(2 * g.n - 1) * g.b * g.b + (long long)g.n * a * g.b;
+  double* v = p.x + base * p.ldx + c;
   const long long ld = p.ldx;
-  if (mode == 0 && p.has_arrow && partial != nullptr) {
+  if (mode == 0 && g.use_arrow) {
     for (int t = 0; t < a; ++t) {
       double tot = 0.0;
-      for (int g = 0; g < nparts; ++g) tot += partial[((long long)g * a + t) * NRMAX + r];
+      for (int R = 0; R < nparts; ++R) tot += p.part[((long long)R * a + t) * NR + c];
       v[t * ld] -= tot;
     }
   }
   if (mode == 0) {
     for (int t = 0; t < a; ++t) {
       double s = v[t * ld];
-      for (int u = 0; u < t; ++u) s -= p.tip[(long long)t * a + u] * v[u * ld];
-      v[t * ld] = s / p.tip[(long long)t * a + t];
+      for (int u = 0; u < t; ++u) s -= tip[(long long)t * a + u] * v[u * ld];
+      v[t * ld] = s / tip[(long long)t * a + t];
     }
   } else {
     for (int t = a - 1; t >= 0; --t) {
       double s = v[t * ld];
-      for (int u = t + 1; u < a; ++u) s -= p.tip[(long long)u * a + t] * v[u * ld];
-      v[t * ld] = s / p.tip[(long long)t * a + t];
+      for (int u = t + 1; u < a; ++u) s -= tip[(long long)u * a + t] * v[u * ld];
+      v[t * ld] = s / tip[(long long)t * a + t];
     }
   }
-  for (int t = 0; t < a; ++t) xtip[t * NRMAX + r] = v[t * ld];
+  for (int t = 0; t < a; ++t) xtip[t * NR + c] = v[t * ld];
 }
 
 static size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
-static constexpr int ARROW_PARTS = 148 * 2;
 
 struct PobtasWs {
   int* flags;
   int* ticket;
-  double* partial;
+  double* part;
   double* xtip;
+  double* push;
+  double* winv;
 };
 
 static size_t pobtas_ws(int n, int b, int a, char* base, PobtasWs* o) {
-  const int nck = ceil_div(b, CH);
-  size_t off = 0;
-  const size_t f = align_up((size_t)n * nck * sizeof(int));
-  const size_t t = align_up(sizeof(int) * 2);
-  const size_t pa = align_up((size_t)ARROW_PARTS * (a > 0 ? a : 1) * NRMAX * sizeof(double));
-  const size_t xt = align_up((size_t)(a > 0 ? a : 1) * NRMAX * sizeof(double));
+  const int ntile = n * ((b + 127) / 128);
+  const size_t f = align_up((size_t)(ntile + 2) * sizeof(int));
+  const size_t pa = align_up((size_t)ntile * (a > 0 ? a : 1) * NR * sizeof(double));
+  const size_t xt = align_up((size_t)(a > 0 ? a : 1) * NR * sizeof(double));
+  const size_t pu = align_up((size_t)ntile * 128 * NR * sizeof(double));
+  const size_t wi = (size_t)ntile * WPK * sizeof(double);
   if (o) {
     o->flags = reinterpret_cast<int*>(base);
-    o->ticket = reinterpret_cast<int*>(base + f);
-    o->partial = reinterpret_cast<double*>(base + f + t);
-    o->xtip = reinterpret_cast<double*>(base + f + t + pa);
+    o->ticket = o->flags + ntile;
+    o->part = reinterpret_cast<double*>(base + f);
+    o->xtip = reinterpret_cast<double*>(base + f + pa);
+    o->push = reinterpret_cast<double*>(base + f + pa + xt);
+    o->winv = reinterpret_cast<double*>(base + f + pa + xt + pu);
   }
-  off = f + t + pa + xt;
-  return off;
+  return f + pa + xt + pu + wi;
 }
 
-static int run_sweeps(const SweepArgs& base_args, int mode, const PobtasWs& ws, cudaStream_t st) {
-  SweepArgs p = base_args;
-  const int total = p.n * p.nck;
-  const size_t fbytes = (size_t)total * sizeof(int);
+static int run_sweeps(SweepArgs p, int mode, const PobtasWs& ws, cudaStream_t st) {
+  const size_t fbytes = (size_t)(p.ntile + 1) * sizeof(int);  // flags + ticket
+  const size_t smem = PS_SMEM_DOUBLES * sizeof(double);
+  const size_t ismem = INV_SMEM_DOUBLES * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    int e1 = (int)cudaFuncSetAttribute(sweep_kernel<true, 1>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int e2 = (int)cudaFuncSetAttribute(sweep_kernel<false, 1>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    e1 |= (int)cudaFuncSetAttribute(sweep_kernel<true, NR>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    e2 |= (int)cudaFuncSetAttribute(sweep_kernel<false, NR>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int e3 = (int)cudaFuncSetAttribute(inv_tiles_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ismem);
+    if (e1) return e1;
+    if (e2) return e2;
+    if (e3) return e3;
+    attr = true;
+  }
   int e;
+  inv_tiles_kernel<<<p.ntile, PS_NT, ismem, st>>>(p.g, ws.winv);
+  count_launch();
+  if ((e = (int)cudaGetLastError())) return e;
   if (mode == 0 || mode == 1) {
     if ((e = (int)cudaMemsetAsync(p.flags, 0, fbytes, st))) return e;
-    if ((e = (int)cudaMemsetAsync(p.ticket, 0, sizeof(int), st))) return e;
-    fwd_sweep_kernel<<<total, 256, 0, st>>>(p);
+    if (p.ncols == 1) sweep_kernel<true, 1><<<p.ntile, PS_NT, smem, st>>>(p);
+    else sweep_kernel<true, NR><<<p.ntile, PS_NT, smem, st>>>(p);
     count_launch();
     if ((e = (int)cudaGetLastError())) return e;
-    if (p.a > 0) {
-      int parts = 0;
-      if (p.has_arrow) {
-        const long long N = (long long)p.n * p.b;
-        const int cpc = (int)((N + ARROW_PARTS - 1) / ARROW_PARTS);
-        parts = (int)((N + cpc - 1) / cpc);
-        arrow_partial_kernel<<<parts, 256, 0, st>>>(p, ws.partial, cpc);
-        count_launch();
-        if ((e = (int)cudaGetLastError())) return e;
-      }
-      tip_solve_kernel<<<1, NRMAX, 0, st>>>(p, ws.partial, parts, ws.xtip, 0);
+    if (p.g.a > 0) {
+      tip_solve_kernel<<<1, NR, 0, st>>>(p, p.ntile, ws.xtip, 0);
       count_launch();
       if ((e = (int)cudaGetLastError())) return e;
     }
   }
   if (mode == 0 || mode == 2) {
-    if (p.a > 0) {
-      tip_solve_kernel<<<1, NRMAX, 0, st>>>(p, nullptr, 0, ws.xtip, 1);
+    if (p.g.a > 0) {
+      tip_solve_kernel<<<1, NR, 0, st>>>(p, 0, ws.xtip, 1);
       count_launch();
       if ((e = (int)cudaGetLastError())) return e;
     }
     if ((e = (int)cudaMemsetAsync(p.flags, 0, fbytes, st))) return e;
-    if ((e = (int)cudaMemsetAsync(p.ticket, 0, sizeof(int), st))) return e;
-    bwd_sweep_kernel<<<total, 256, 0, st>>>(p, ws.xtip);
+    if (p.ncols == 1) sweep_kernel<false, 1><<<p.ntile, PS_NT, smem, st>>>(p);
+    else sweep_kernel<false, NR><<<p.ntile, PS_NT, smem, st>>>(p);
     count_launch();
     if ((e = (int)cudaGetLastError())) return e;
   }
@@ -419,28 +534,35 @@ size_t stbta_pobtas_workspace_bytes(int n, int b, int a, int nrhs) {
 
 int stbta_pobtas(const double* factor, int n, int b, int a, int has_arrow, double* rhs, int nrhs,
                  int mode, void* workspace, size_t workspace_bytes, void* stream) {
-  if (factor == nullptr || rhs == nullptr || n < 1 || b < 1 || a < 0 ||
-      nrhs < 1 || mode < 0 || mode > 2)
+  if (factor == nullptr || rhs == nullptr || n < 1 || b < 1 || a < 0 || nrhs < 1 || mode < 0 ||
+      mode > 2)
     return STBTA_EARG;
   if (workspace_bytes < stbta_pobtas_workspace_bytes(n, b, a, nrhs)) return STBTA_EWORKSPACE;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   PobtasWs ws;
   pobtas_ws(n, b, a, reinterpret_cast<char*>(workspace), &ws);
-  const long long bb = (long long)b * b;
   SweepArgs p{};
-  p.diag = factor;
-  p.lower = factor + n * bb;
-  p.arrow = p.lower + (long long)(n - 1) * bb;
-  p.tip = p.arrow + (long long)n * a * b;
-  p.n = n; p.b = b; p.a = a;
-  p.nck = ceil_div(b, CH);
-  p.has_arrow = has_arrow && a > 0;
+  Band& g = p.g;
+  g.data = const_cast<double*>(factor);
+  g.n = n; g.b = b; g.a = a;
+  g.nbt = (b + 127) / 128;
+  g.nat = a > 0 ? (a + 127) / 128 : 0;
+  g.S = n * g.nbt + g.nat;
+  g.use_arrow = has_arrow && a > 0;
+  g.vec_b = 0;
+  g.vec_a = 0;
+  p.ntile = n * g.nbt;
   p.ldx = nrhs;
   p.flags = ws.flags;
   p.ticket = ws.ticket;
-  for (int c0 = 0; c0 < nrhs; c0 += NRMAX) {
+  p.part = ws.part;
+  p.xtip = ws.xtip;
+  p.push = ws.push;
+  p.winv = ws.winv;
+  p.prof = debug_profile();
+  for (int c0 = 0; c0 < nrhs; c0 += NR) {
     p.x = rhs + c0;
-    p.ncols = nrhs - c0 < NRMAX ? nrhs - c0 : NRMAX;
+    p.ncols = nrhs - c0 < NR ? nrhs - c0 : NR;
     int e = run_sweeps(p, mode, ws, st);
     if (e) return e;
   }

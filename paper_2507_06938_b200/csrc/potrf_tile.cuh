@@ -64,6 +64,30 @@ STBTA_DEV void mma4x4(double (&acc)[4][4], const double* a, int lda, const doubl
   }
 }
 
+// Conflict-free SIMT product on a 32x32 output block by 64 threads: thread
+// (tr, tc) = (id & 7, id >> 3) owns rows tr + 8i and cols tc + 8j, i, j < 4,
+// so a warp's A loads touch 8 consecutive rows (odd row stride: distinct
+// banks) and its B loads 4 distinct rows (broadcast).
+// acc[i][j] = sum_k A[tr+8i][k] * B(k, tc+8j), A row-major (lda), B(k, n) =
+// b[n * ldb + k] (BT) or b[k * ldb + n].
+template <int K, bool BT>
+STBTA_DEV void mma32_blk(double (&acc)[4][4], const double* a, int lda, const double* b, int ldb,
+                         int id) {
+  const int tr = id & 7, tc = id >> 3;
+#pragma unroll 4
+  for (int k = 0; k < K; ++k) {
+    double av[4], bv[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) av[i] = a[(tr + 8 * i) * lda + k];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) bv[j] = BT ? b[(tc + 8 * j) * ldb + k] : b[k * ldb + tc + 8 * j];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[i][j] = fma(av[i], bv[j], acc[i][j]);
+  }
+}
+
 STBTA_DEV void zero4x4(double (&acc)[4][4]) {
 #pragma unroll
   for (int i = 0; i < 4; ++i)
@@ -159,42 +183,45 @@ STBTA_DEV int potrf_tile_smem(double* T, double* WT, double* scratch, double* lo
     if (*s_fail) return 1;
     const int rem = 96 - k0;  // rows below the diagonal block
     if (rem == 0) break;
-    // ---- TRSM: L_ik = A_ik W_kk^T for rows [k0+32, 128): C[r][j] = sum_l A[r][l] WT[l][j]
+    // ---- TRSM: L_ik = A_ik W_kk^T for rows [k0+32, 128) (32x32 blocks, 64 threads each)
     {
-      const int ntile = (rem / 4) * 8;  // 4x4 micro-tiles: rem/4 rows x 8 cols
+      const int nblk = rem / 32;
+      const int blk = tid >> 6, id = tid & 63;
       double acc[4][4];
       zero4x4(acc);
-      const int mr = (tid >> 3) * 4, nc = (tid & 7) * 4;
-      if (tid < ntile)
-        mma4x4<32, false>(acc, T + (k0 + 32 + mr) * PT_LD + k0, PT_LD,
-                          WT + kb * 32 * PT_WLD + nc, PT_WLD);
+      if (blk < nblk)
+        mma32_blk<32, false>(acc, T + (k0 + 32 + blk * 32) * PT_LD + k0, PT_LD,
+                             WT + kb * 32 * PT_WLD, PT_WLD, id);
       __syncthreads();
-      if (tid < ntile) {
+      if (blk < nblk) {
+        const int tr = id & 7, tc = id >> 3;
+        double* d = T + (k0 + 32 + blk * 32) * PT_LD + k0;
 #pragma unroll
         for (int i = 0; i < 4; ++i)
 #pragma unroll
-          for (int j = 0; j < 4; ++j) T[(k0 + 32 + mr + i) * PT_LD + k0 + nc + j] = acc[i][j];
+          for (int j = 0; j < 4; ++j) d[(tr + 8 * i) * PT_LD + tc + 8 * j] = acc[i][j];
       }
     }
     __syncthreads();
     stamp(1);
-    // ---- trailing update: A_rc -= L_r L_c^T on lower 4x4 micro-tiles
+    // ---- trailing update: A_rc -= L_r L_c^T on lower 32x32 blocks (64 threads each)
     {
-      const int nt4 = rem / 4;
-      const int ntile = nt4 * (nt4 + 1) / 2;
+      const int nb = rem / 32;
+      const int nblk = nb * (nb + 1) / 2;
       const double* base = T + (k0 + 32) * PT_LD + k0;
 #pragma unroll 1
-      for (int tix = tid; tix < ntile; tix += NT) {
-        int tr, tc;
-        tri_decode(tix, &tr, &tc);
+      for (int blk = tid >> 6; blk < nblk; blk += NT / 64) {
+        int br, bc;
+        tri_decode(blk, &br, &bc);
+        const int id = tid & 63, tr = id & 7, tc = id >> 3;
         double acc[4][4];
         zero4x4(acc);
-        mma4x4<32, true>(acc, base + tr * 4 * PT_LD, PT_LD, base + tc * 4 * PT_LD, PT_LD);
-        double* d = T + (k0 + 32 + tr * 4) * PT_LD + k0 + 32 + tc * 4;
+        mma32_blk<32, true>(acc, base + br * 32 * PT_LD, PT_LD, base + bc * 32 * PT_LD, PT_LD, id);
+        double* d = T + (k0 + 32 + br * 32) * PT_LD + k0 + 32 + bc * 32;
 #pragma unroll
         for (int i = 0; i < 4; ++i)
 #pragma unroll
-          for (int j = 0; j < 4; ++j) d[i * PT_LD + j] -= acc[i][j];
+          for (int j = 0; j < 4; ++j) d[(tr + 8 * i) * PT_LD + tc + 8 * j] -= acc[i][j];
       }
     }
     __syncthreads();

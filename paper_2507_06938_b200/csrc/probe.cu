@@ -11,6 +11,8 @@ namespace stbta {
 
 static std::atomic<long long> g_launches{0};
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+static unsigned long long* g_prof = nullptr;
+unsigned long long* debug_profile() { return g_prof; }
 
 __global__ void __launch_bounds__(256) dmma_probe_kernel(int iters, double* out) {
   constexpr int ACC = 16;
@@ -75,6 +77,8 @@ int stbta_debug_latency(int which, int iters, double* scratch, long long* cycles
 }
 
 long long stbta_launch_count(void) { return stbta::g_launches.load(); }
+// Debug hook: see include/stbta.h.
+void stbta_debug_set_profile(unsigned long long* buf) { stbta::g_prof = buf; }
 // blocks x 256 threads, each thread iters*8 DFMA.  FLOPs = blocks*256*iters*16.
 int stbta_probe_dfma(int blocks, int iters, double* scratch, void* stream) {
   stbta::dfma_probe_kernel<<<blocks, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(iters,

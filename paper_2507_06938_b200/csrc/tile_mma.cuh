@@ -21,26 +21,27 @@ struct Opnd {
   int vec;   // 16-byte copies allowed
 };
 
-template <int BM_, int BN_, int WM_, int WN_, int NT_>
+template <int BM_, int BN_, int WM_, int WN_, int NT_, int BK_ = 16, int ST_ = 4>
 struct MmaCfg {
   static constexpr int BM = BM_, BN = BN_, WM = WM_, WN = WN_, NT = NT_;
   static constexpr int WARPS_M = BM / WM, WARPS_N = BN / WN;
   static_assert(WARPS_M * WARPS_N * 32 == NT, "warp layout must cover the CTA");
   static constexpr int MF = WM / 8, NF = WN / 8;
-  static constexpr int BK = 16, STAGES = 4, LDS = BK + 4;
+  static constexpr int BK = BK_, STAGES = ST_, LDS = BK + 4;
   static constexpr int A_STAGE = BM * LDS, B_STAGE = BN * LDS;
   static constexpr int SMEM_DOUBLES = STAGES * (A_STAGE + B_STAGE);
 };
 
-template <int ROWS, int NT>
+template <int ROWS, int NT, int BK = 16>
 STBTA_DEV void load_slab(double* sm, const Opnd& o, int k0, int K) {
-  constexpr int LDS = 16 + 4;
+  constexpr int LDS = BK + 4;
+  constexpr int HP = BK / 2;  // 16-byte pairs per row
   const int tid = threadIdx.x;
   if (o.vec) {
-    constexpr int PAIRS = ROWS * 8;
+    constexpr int PAIRS = ROWS * HP;
 #pragma unroll
     for (int e = tid; e < PAIRS; e += NT) {
-      const int r = e >> 3, c = (e & 7) * 2;
+      const int r = e / HP, c = (e % HP) * 2;
       const int gc = k0 + c;
       int bytes = 0;
       const double* src = o.p;
@@ -51,10 +52,10 @@ STBTA_DEV void load_slab(double* sm, const Opnd& o, int k0, int K) {
       cp_async16(sm + r * LDS + c, src, bytes);
     }
   } else {
-    constexpr int ELEMS = ROWS * 16;
+    constexpr int ELEMS = ROWS * BK;
 #pragma unroll
     for (int e = tid; e < ELEMS; e += NT) {
-      const int r = e >> 4, c = e & 15;
+      const int r = e / BK, c = e % BK;
       const int gc = k0 + c;
       const bool ok = r < o.rows && gc < K;
       cp_async8(sm + r * LDS + c, ok ? o.p + (long long)r * o.ld + gc : o.p, ok);
@@ -66,7 +67,7 @@ STBTA_DEV void load_slab(double* sm, const Opnd& o, int k0, int K) {
 // column is >= n_active skip the arithmetic (triangular strips).  All threads
 // of the CTA must call; smem holds Cfg::SMEM_DOUBLES doubles.  Ends with a
 // __syncthreads so the caller may reuse shared memory.
-template <class Cfg, bool NEG = false>
+template <class Cfg, bool NEG = false, int DBG = 0>
 STBTA_DEV void tile_mma(double (&acc)[Cfg::MF][Cfg::NF][2], const Opnd& A, const Opnd& B, int K,
                         int n_active, double* smem) {
   constexpr int MF = Cfg::MF, NF = Cfg::NF, BK = Cfg::BK, ST = Cfg::STAGES, LDS = Cfg::LDS;
@@ -82,18 +83,20 @@ STBTA_DEV void tile_mma(double (&acc)[Cfg::MF][Cfg::NF][2], const Opnd& A, const
 #pragma unroll
   for (int s = 0; s < ST - 1; ++s) {
     if (s < ktiles) {
-      load_slab<Cfg::BM, Cfg::NT>(As + s * Cfg::A_STAGE, A, s * BK, K);
-      load_slab<Cfg::BN, Cfg::NT>(Bs + s * Cfg::B_STAGE, B, s * BK, K);
+      load_slab<Cfg::BM, Cfg::NT, Cfg::BK>(As + s * Cfg::A_STAGE, A, s * BK, K);
+      load_slab<Cfg::BN, Cfg::NT, Cfg::BK>(Bs + s * Cfg::B_STAGE, B, s * BK, K);
     }
     cp_async_commit();
   }
   for (int kt = 0; kt < ktiles; ++kt) {
-    cp_async_wait<ST - 2>();
-    __syncthreads();
+    if (DBG != 1) {  // DBG 1: no waits/barriers (timing experiment only)
+      cp_async_wait<ST - 2>();
+      __syncthreads();
+    }
     const int nt = kt + ST - 1;
-    if (nt < ktiles) {
-      load_slab<Cfg::BM, Cfg::NT>(As + (nt % ST) * Cfg::A_STAGE, A, nt * BK, K);
-      load_slab<Cfg::BN, Cfg::NT>(Bs + (nt % ST) * Cfg::B_STAGE, B, nt * BK, K);
+    if (DBG != 2 && nt < ktiles) {  // DBG 2: no loads in the main loop
+      load_slab<Cfg::BM, Cfg::NT, Cfg::BK>(As + (nt % ST) * Cfg::A_STAGE, A, nt * BK, K);
+      load_slab<Cfg::BN, Cfg::NT, Cfg::BK>(Bs + (nt % ST) * Cfg::B_STAGE, B, nt * BK, K);
     }
     cp_async_commit();
     if (active) {
@@ -176,6 +179,128 @@ STBTA_DEV void acc_store(const double (&acc)[Cfg::MF][Cfg::NF][2], double* C, lo
       }
     }
   }
+}
+
+}  // namespace stbta
+
+// ---------------------------------------------------------------------------
+// Bulk-copy variant for full tiles (rows == BM/BN, K % BK == 0, 16-byte rows):
+// warp 0 streams each BK-wide row segment with one cp.async.bulk (TMA engine,
+// completion counted on a per-stage "full" mbarrier); warps release a stage
+// on its "empty" mbarrier, so there is no CTA-wide barrier per K slab and the
+// load issue costs 8 instructions per lane per slab instead of ~20 per thread.
+// `slab` is the CTA's running slab counter (identical in every thread); it
+// selects stage = slab % ST and the mbarrier parities, so the ring carries
+// over from one task to the next.
+namespace stbta {
+
+STBTA_DEV unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+
+STBTA_DEV void mbar_init(unsigned long long* bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+STBTA_DEV void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+STBTA_DEV void mbar_arrive(unsigned long long* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+STBTA_DEV void mbar_wait(unsigned long long* bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+STBTA_DEV void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+STBTA_DEV void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+
+// bars: 2*ST mbarriers (full[0..ST), empty[ST..2ST)), initialised with
+// full = 1 arrival, empty = NT/32 arrivals, before the first use.
+template <class Cfg>
+STBTA_DEV void bulk_bars_init(unsigned long long* bars) {
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < Cfg::STAGES; ++s) {
+      mbar_init(bars + s, 1);
+      mbar_init(bars + Cfg::STAGES + s, Cfg::NT / 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+}
+
+template <class Cfg, bool NEG = false>
+STBTA_DEV void tile_mma_bulk(double (&acc)[Cfg::MF][Cfg::NF][2], const double* A, long long lda,
+                             const double* B, long long ldb, int K, double* smem,
+                             unsigned long long* bars, unsigned& slab) {
+  constexpr int MF = Cfg::MF, NF = Cfg::NF, BK = Cfg::BK, ST = Cfg::STAGES, LDS = Cfg::LDS;
+  constexpr unsigned ROWB = BK * 8;
+  constexpr unsigned STAGE_TX = (Cfg::BM + Cfg::BN) * ROWB;
+  double* As = smem;
+  double* Bs = smem + ST * Cfg::A_STAGE;
+  unsigned long long* full = bars;
+  unsigned long long* empty = bars + ST;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gq = lane >> 2, tq = lane & 3;
+  const int wm0 = (warp % Cfg::WARPS_M) * Cfg::WM;
+  const int wn0 = (warp / Cfg::WARPS_M) * Cfg::WN;
+  const int nslab = K / BK;
+
+  auto produce = [&](int i) {  // warp 0 only
+    const unsigned c = slab + i;
+    const int st = c % ST;
+    if (c >= ST) mbar_wait(empty + st, ((c / ST) - 1) & 1);
+    if (lane == 0) mbar_expect_tx(full + st, STAGE_TX);
+    __syncwarp();
+    const int k0 = i * BK;
+    for (int r = lane; r < Cfg::BM; r += 32)
+      bulk_g2s(As + st * Cfg::A_STAGE + r * LDS, A + (long long)r * lda + k0, ROWB, full + st);
+    for (int r = lane; r < Cfg::BN; r += 32)
+      bulk_g2s(Bs + st * Cfg::B_STAGE + r * LDS, B + (long long)r * ldb + k0, ROWB, full + st);
+  };
+
+  if (warp == 0) {
+    fence_proxy_async();  // smem last written through the generic proxy
+    const int pre = nslab < ST ? nslab : ST;
+    for (int i = 0; i < pre; ++i) produce(i);
+  }
+  for (int i = 0; i < nslab; ++i) {
+    const unsigned c = slab + i;
+    const int st = c % ST;
+    mbar_wait(full + st, (c / ST) & 1);
+    const double* as = As + st * Cfg::A_STAGE;
+    const double* bs = Bs + st * Cfg::B_STAGE;
+#pragma unroll
+    for (int ks = 0; ks < BK / 4; ++ks) {
+      const int k = ks * 4 + tq;
+      double af[MF], bf[NF];
+#pragma unroll
+      for (int ii = 0; ii < MF; ++ii) af[ii] = as[(wm0 + ii * 8 + gq) * LDS + k];
+#pragma unroll
+      for (int j = 0; j < NF; ++j)
+        bf[j] = NEG ? -bs[(wn0 + j * 8 + gq) * LDS + k] : bs[(wn0 + j * 8 + gq) * LDS + k];
+#pragma unroll
+      for (int ii = 0; ii < MF; ++ii)
+#pragma unroll
+        for (int j = 0; j < NF; ++j) dmma884(acc[ii][j][0], acc[ii][j][1], af[ii], bf[j]);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty + st);
+    if (warp == 0 && i + ST < nslab) produce(i + ST);
+  }
+  slab += nslab;
 }
 
 }  // namespace stbta
