@@ -55,20 +55,13 @@ struct SweepArgs {
 };
 
 // ---------------------------------------------------------------- pre-pass
-// W_R = L_RR^-1 for every diagonal tile, packed lower (row-major).  Blocked:
-// warp kb inverts the 32x32 diagonal block kb (one column per lane), then the
-// off-diagonal blocks by diagonals, W_ij = -W_ii sum_{k=j}^{i-1} L_ik W_kj.
-constexpr int INV_LD = 129, BLD = 33;
-constexpr int INV_SMEM_DOUBLES = 128 * INV_LD + 11 * 32 * BLD;
-
+// W_R = L_RR^-1 for every diagonal tile, packed lower (row-major), through
+// the in-CTA blocked inversion of potrf_tile.cuh.
 __global__ void __launch_bounds__(PS_NT, 1) inv_tiles_kernel(Band g, double* winv) {
   extern __shared__ __align__(16) double sm[];
-  double* T = sm;                       // L lower; W_ij^T (i > j) in upper block (j, i)
-  double* WT = T + 128 * INV_LD;        // W_kk^T: WT[kb][c][i] = W_kk[i][c]
-  double* Wd = WT + 4 * 32 * BLD;       // W_kk row-major
-  double* TS = Wd + 4 * 32 * BLD;       // scratch products, 3 blocks
+  double* T = sm;
   const int R = blockIdx.x;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int tid = threadIdx.x;
   const int ext = tile_extent(g, R);
   const TilePtr tp = tile_ptr(g, R, R);
   for (int e = tid; e < 128 * 128; e += PS_NT) {
@@ -79,67 +72,13 @@ __global__ void __launch_bounds__(PS_NT, 1) inv_tiles_kernel(Band g, double* win
     T[r * INV_LD + c] = v;
   }
   __syncthreads();
-  if (warp < 4) {
-    const int k0 = warp * 32;
-    double* dinv = TS + warp * 32;
-    dinv[lane] = 1.0 / T[(k0 + lane) * INV_LD + k0 + lane];
-    __syncwarp();
-    double w[32];
-#pragma unroll
-    for (int i = 0; i < 32; ++i) w[i] = (i == lane) ? 1.0 : 0.0;
-#pragma unroll 32
-    for (int k = 0; k < 32; ++k) {
-      w[k] *= dinv[k];
-#pragma unroll 32
-      for (int i = k + 1; i < 32; ++i) w[i] = fma(-T[(k0 + i) * INV_LD + k0 + k], w[k], w[i]);
-    }
-#pragma unroll
-    for (int i = 0; i < 32; ++i) {
-      WT[warp * 32 * BLD + lane * BLD + i] = w[i];
-      Wd[warp * 32 * BLD + i * BLD + lane] = w[i];
-    }
-  }
-  __syncthreads();
-  for (int d = 1; d < 4; ++d) {
-    const int nb = 4 - d, blk = tid >> 6, id = tid & 63, tr = id & 7, tc = id >> 3;
-    if (blk < nb) {  // T_j = sum_k L_ik W_kj  (i = j + d)
-      const int j = blk, i = j + d;
-      double acc[4][4];
-      zero4x4(acc);
-      for (int k = j; k < i; ++k) {
-        const double* b = (k == j) ? WT + j * 32 * BLD : T + (32 * j) * INV_LD + 32 * k;
-        const int ldb = (k == j) ? BLD : INV_LD;
-        mma32_blk<32, true>(acc, T + (32 * i) * INV_LD + 32 * k, INV_LD, b, ldb, id);
-      }
-#pragma unroll
-      for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int c = 0; c < 4; ++c) TS[j * 32 * BLD + (tr + 8 * a) * BLD + tc + 8 * c] = acc[a][c];
-    }
-    __syncthreads();
-    if (blk < nb) {  // W_ij = -W_ii T_j, stored transposed into T's upper block (j, i)
-      const int j = blk, i = j + d;
-      double acc[4][4];
-      zero4x4(acc);
-      mma32_blk<32, false>(acc, Wd + i * 32 * BLD, BLD, TS + j * 32 * BLD, BLD, id);
-#pragma unroll
-      for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int c = 0; c < 4; ++c)
-          T[(32 * j + tc + 8 * c) * INV_LD + 32 * i + tr + 8 * a] = -acc[a][c];
-    }
-    __syncthreads();
-  }
+  invert_tile_smem<PS_NT>(sm);
   double* out = winv + (long long)R * WPK;
   for (int e = tid; e < WPK; e += PS_NT) {
     int r = (int)((sqrtf(8.0f * e + 1.0f) - 1.0f) * 0.5f);
     if ((r + 1) * (r + 2) / 2 <= e) ++r;
     if (r * (r + 1) / 2 > e) --r;
-    const int c = e - r * (r + 1) / 2;
-    double v;
-    if ((r >> 5) == (c >> 5)) v = Wd[(r >> 5) * 32 * BLD + (r & 31) * BLD + (c & 31)];
-    else v = T[c * INV_LD + r];
-    out[e] = v;
+    out[e] = inv_tile_at(sm, r, e - r * (r + 1) / 2);
   }
 }
 

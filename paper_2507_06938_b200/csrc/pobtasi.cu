@@ -5,66 +5,284 @@
 //   X_{i+1,i} = -(X_{i+1,i+1} L_{i+1,i} + X_{a,i+1}^T L_{a,i}) W
 //   X_{a,i}   = -(X_tip L_{a,i} + X_{a,i+1} L_{i+1,i}) W
 //   X_{i,i}   = (W^T - X_{i+1,i}^T L_{i+1,i} - X_{a,i}^T L_{a,i}) W
-// Every product is one DMMA engine launch (NN / TN, with W's triangle used to
-// bound the K range), W comes from the recursive TRTRI (dense.cu).
+//
+// B200 mapping.
+//  1. Every inverse W_i = L_ii^-1 (and the tip's) is computed up front, all
+//     blocks at once, since they do not depend on the recursion: the 128x128
+//     diagonal tiles are inverted in-CTA (potrf_tile.cuh), then the
+//     off-diagonal tiles diagonal by diagonal, W_rc = -W_rr sum_k L_rk W_kc,
+//     one launch per tile diagonal covering all blocks.
+//  2. The recursion is then a chain of full-size FP64 DMMA tile GEMMs (one CTA
+//     per 128x128 output tile, K streamed through a cp.async ring, operands in
+//     either storage orientation so no transposes are materialised), with the
+//     triangular structure of W used to skip the zero K-range and X_ii formed
+//     on its lower tiles and mirrored.
 #include "../../include/stbta.h"
+#include "band.cuh"
+#include "potrf_tile.cuh"
 #include "stbta_internal.cuh"
+#include "tile_mma.cuh"
 
 namespace stbta {
 
-// out (n x n, ld_out) = in^T (n x n, ld_in)
-__global__ void transpose_kernel(const double* __restrict__ in, long long ld_in, double* out,
-                                 long long ld_out, int n, const int* info) {
-  __shared__ double t[32][33];
-  if (info != nullptr && *info != 0) return;
-  const int bx = blockIdx.x * 32, by = blockIdx.y * 32;
-  for (int r = threadIdx.y; r < 32; r += 8) {
-    const int gr = by + r, gc = bx + threadIdx.x;
-    if (gr < n && gc < n) t[r][threadIdx.x] = in[(long long)gr * ld_in + gc];
+constexpr int SI_NT = 256;
+using SiCfg = MmaCfg<128, 128, 64, 32, SI_NT, 16, 4>;
+constexpr int SI_SMEM_DOUBLES =
+    SiCfg::SMEM_DOUBLES > INV_SMEM_DOUBLES ? SiCfg::SMEM_DOUBLES : INV_SMEM_DOUBLES;
+
+// one product of a tile job: acc += sgn * sum_k A(m, k) B(n, k) for k in
+// [kbeg, K), A(m,k) = akm ? A[k*lda + m] : A[m*lda + k] (B likewise); ktri:
+// kbeg = first column of the output tile (B is lower-triangular W^T-like).
+struct Prod {
+  const double* A;
+  long long lda;
+  const double* B;
+  long long ldb;
+  int K, akm, bkm, ktri, arows_all;
+  double sgn;
+};
+
+struct TileJob {
+  double* C;
+  long long ldc;
+  int M, N;
+  int init;        // 0: zero, 1: acc = C, 2: acc[m][n] = ci[n][m] (transposed init)
+  const double* ci;
+  long long ldci;
+  double alpha;    // C = alpha * acc
+  int lower;       // only tiles with tr >= tc
+  int mirror;      // also write the transposed tile to (tc, tr)
+  int nprod;
+  Prod p[2];
+};
+
+template <bool AKM, bool BKM>
+STBTA_DEV void run_prod(double (&acc)[SiCfg::MF][SiCfg::NF][2], const Prod& p, int tr, int tc,
+                        int mrows, int ncols, double* smem) {
+  const Opnd A{AKM ? p.A + tr * 128 : p.A + (long long)tr * 128 * p.lda, p.lda,
+               p.arows_all ? 128 : mrows, 0};
+  const Opnd B{BKM ? p.B + tc * 128 : p.B + (long long)tc * 128 * p.ldb, p.ldb, ncols, 0};
+  Opnd a = A, b = B;
+  a.vec = ((uintptr_t)a.p % 16 == 0) && (a.ld % 2 == 0);
+  b.vec = ((uintptr_t)b.p % 16 == 0) && (b.ld % 2 == 0);
+  const int kbeg = p.ktri ? tc * 128 : 0;
+  if (kbeg >= p.K) return;
+  tile_mma<SiCfg, false, 0, AKM, BKM>(acc, a, b, p.K, 128, smem, kbeg);
+}
+
+STBTA_DEV void acc_neg(double (&acc)[SiCfg::MF][SiCfg::NF][2]) {
+#pragma unroll
+  for (int i = 0; i < SiCfg::MF; ++i)
+#pragma unroll
+    for (int j = 0; j < SiCfg::NF; ++j) acc[i][j][0] = -acc[i][j][0], acc[i][j][1] = -acc[i][j][1];
+}
+
+STBTA_DEV void tile_job_body(const TileJob& j, int tr, int tc, double* smem) {
+  const int mrows = min(128, j.M - tr * 128), ncols = min(128, j.N - tc * 128);
+  double acc[SiCfg::MF][SiCfg::NF][2];
+  if (j.init == 1) {
+    acc_load<SiCfg>(acc, j.C + (long long)tr * 128 * j.ldc + tc * 128, j.ldc, mrows, ncols, 0, 0);
+  } else if (j.init == 2) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, gq = lane >> 2, tq = lane & 3;
+    const int wm0 = (warp % SiCfg::WARPS_M) * SiCfg::WM, wn0 = (warp / SiCfg::WARPS_M) * SiCfg::WN;
+#pragma unroll
+    for (int i = 0; i < SiCfg::MF; ++i)
+#pragma unroll
+      for (int jj = 0; jj < SiCfg::NF; ++jj)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int m = wm0 + i * 8 + gq, n = wn0 + jj * 8 + 2 * tq + e;
+          // ci is lower triangular: element (tc*128+n, tr*128+m) vanishes above its diagonal
+          acc[i][jj][e] = (m < mrows && n < ncols && tc * 128 + n >= tr * 128 + m)
+                              ? __ldcg(j.ci + (long long)(tc * 128 + n) * j.ldci + tr * 128 + m)
+                              : 0.0;
+        }
+  } else {
+    acc_zero<SiCfg>(acc);
+  }
+  for (int q = 0; q < j.nprod; ++q) {
+    const Prod& p = j.p[q];
+    if (p.sgn < 0) acc_neg(acc);
+    if (p.akm && p.bkm) run_prod<true, true>(acc, p, tr, tc, mrows, ncols, smem);
+    else if (p.akm) run_prod<true, false>(acc, p, tr, tc, mrows, ncols, smem);
+    else if (p.bkm) run_prod<false, true>(acc, p, tr, tc, mrows, ncols, smem);
+    else run_prod<false, false>(acc, p, tr, tc, mrows, ncols, smem);
+    if (p.sgn < 0) acc_neg(acc);
+  }
+  acc_store<SiCfg>(acc, j.C + (long long)tr * 128 * j.ldc + tc * 128, j.ldc, mrows, ncols, 0, 0, 0,
+                   j.alpha);
+  if (j.mirror && tr != tc) {  // transposed copy to tile (tc, tr)
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, gq = lane >> 2, tq = lane & 3;
+    const int wm0 = (warp % SiCfg::WARPS_M) * SiCfg::WM, wn0 = (warp / SiCfg::WARPS_M) * SiCfg::WN;
+    double* Ct = j.C + (long long)tc * 128 * j.ldc + tr * 128;
+#pragma unroll
+    for (int i = 0; i < SiCfg::MF; ++i)
+#pragma unroll
+      for (int jj = 0; jj < SiCfg::NF; ++jj)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int m = wm0 + i * 8 + gq, n = wn0 + jj * 8 + 2 * tq + e;
+          if (m < mrows && n < ncols) Ct[(long long)n * j.ldc + m] = j.alpha * acc[i][jj][e];
+        }
+  }
+}
+
+__global__ void __launch_bounds__(SI_NT, 1) tile_job_kernel(TileJob j, int tiles_n) {
+  extern __shared__ __align__(16) double smem[];
+  int t = blockIdx.x;
+  int tr, tc;
+  if (j.lower) {  // lower-triangular tile index
+    tr = (int)((sqrtf(8.0f * t + 1.0f) - 1.0f) * 0.5f);
+    if ((tr + 1) * (tr + 2) / 2 <= t) ++tr;
+    if (tr * (tr + 1) / 2 > t) --tr;
+    tc = t - tr * (tr + 1) / 2;
+  } else {
+    tr = t / tiles_n;
+    tc = t % tiles_n;
+  }
+  tile_job_body(j, tr, tc, smem);
+}
+
+// ------------------------------------------------------- inverses W_i, W_tip
+// Matrix z < nm: lower-triangular L at Lp(z) (ld, size), inverse written to
+// Wp(z) (same ld).  z < n: diagonal block i of the factor; z == n: the tip.
+struct InvSet {
+  const double* L;  // factor base (diag blocks)
+  double* W;        // W_all: n blocks of b x b
+  const double* Lt; // tip factor (a x a)
+  double* Wt;       // tip inverse (a x a)
+  int n, b, a;
+  double* tmp;      // per (matrix, column tile) scratch tile, 128 x 128
+  int ntb;          // tiles per block dim = ceil(b / 128)
+};
+
+STBTA_DEV void inv_mat(const InvSet& s, int z, const double** L, double** W, int* ld, int* size) {
+  if (z < s.n) {
+    *L = s.L + (long long)z * s.b * s.b;
+    *W = s.W + (long long)z * s.b * s.b;
+    *ld = s.b;
+    *size = s.b;
+  } else {
+    *L = s.Lt;
+    *W = s.Wt;
+    *ld = s.a;
+    *size = s.a;
+  }
+}
+
+// diagonal tiles: grid (ntb, nm)
+__global__ void __launch_bounds__(SI_NT, 1) inv_diag_tiles_kernel(InvSet s) {
+  extern __shared__ __align__(16) double sm[];
+  const double* L;
+  double* W;
+  int ld, size;
+  inv_mat(s, blockIdx.y, &L, &W, &ld, &size);
+  const int t = blockIdx.x;
+  if (t * 128 >= size) return;
+  const int ext = min(128, size - t * 128);
+  const double* Lp = L + (long long)t * 128 * ld + t * 128;
+  double* Wp = W + (long long)t * 128 * ld + t * 128;
+  for (int e = threadIdx.x; e < 128 * 128; e += SI_NT) {
+    const int r = e >> 7, c = e & 127;
+    double v;
+    if (r < ext && c < ext) v = (c <= r) ? __ldg(Lp + (long long)r * ld + c) : 0.0;
+    else v = (r == c) ? 1.0 : 0.0;
+    sm[r * INV_LD + c] = v;
   }
   __syncthreads();
-  for (int r = threadIdx.y; r < 32; r += 8) {
-    const int gr = bx + r, gc = by + threadIdx.x;
-    if (gr < n && gc < n) out[(long long)gr * ld_out + gc] = t[threadIdx.x][r];
+  invert_tile_smem<SI_NT>(sm);
+  for (int e = threadIdx.x; e < ext * ext; e += SI_NT) {
+    const int r = e / ext, c = e % ext;
+    Wp[(long long)r * ld + c] = inv_tile_at(sm, r, c);
   }
+}
+
+// tile diagonal d >= 1: CTA (c, z) forms T = sum_{k=c}^{r-1} L_rk W_kc (r = c+d)
+// into its scratch tile, then W_rc = -W_rr T.
+__global__ void __launch_bounds__(SI_NT, 1) inv_offdiag_kernel(InvSet s, int d) {
+  extern __shared__ __align__(16) double smem[];
+  const double* L;
+  double* W;
+  int ld, size;
+  const int z = blockIdx.y;
+  inv_mat(s, z, &L, &W, &ld, &size);
+  const int ntiles = (size + 127) / 128;
+  const int c = blockIdx.x, r = c + d;
+  if (r >= ntiles) return;
+  const int er = min(128, size - r * 128), ec = min(128, size - c * 128);
+  double* T = s.tmp + ((long long)z * s.ntb + c) * 128 * 128;
+  double acc[SiCfg::MF][SiCfg::NF][2];
+  acc_zero<SiCfg>(acc);
+  {
+    // A(m, k) = L[r*128 + m][k], k in [c*128, r*128);  B(n, k) = W[k][c*128 + n]
+    Opnd A{L + (long long)r * 128 * ld, ld, er, 0};
+    Opnd B{W + c * 128, ld, ec, 0};
+    A.vec = ((uintptr_t)A.p % 16 == 0) && (ld % 2 == 0);
+    B.vec = ((uintptr_t)B.p % 16 == 0) && (ld % 2 == 0);
+    tile_mma<SiCfg, false, 0, false, true>(acc, A, B, r * 128, 128, smem, c * 128);
+  }
+  acc_store<SiCfg>(acc, T, 128, 128, 128, 0, 0, 0, 1.0);
+  __syncthreads();
+  acc_zero<SiCfg>(acc);
+  {
+    // A = W_rr (er x er), B(n, k) = T[k][n]
+    Opnd A{W + (long long)r * 128 * ld + r * 128, ld, er, 0};
+    Opnd B{T, 128, ec, 1};
+    A.vec = ((uintptr_t)A.p % 16 == 0) && (ld % 2 == 0);
+    tile_mma<SiCfg, false, 0, false, true>(acc, A, B, er, 128, smem, 0);
+  }
+  acc_store<SiCfg>(acc, W + (long long)r * 128 * ld + c * 128, ld, er, ec, 0, 0, 0, -1.0);
 }
 
 static size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 
 struct PobtasiWs {
-  double *W, *T1, *tmp, *T2, *winv, *Wt;
+  double *Wall, *Wt, *T1, *T3, *Ta, *tmp;
 };
 
 static size_t pobtasi_ws(int n, int b, int a, char* base, PobtasiWs* o) {
-  (void)n;
+  const int ntb = (b + 127) / 128;
+  const int nta = a > 0 ? (a + 127) / 128 : 0;
+  const int ntm = ntb > nta ? ntb : nta;
+  const size_t wall = align_up((size_t)n * b * b * sizeof(double));
+  const size_t wt = align_up((size_t)(a > 0 ? a * a : 1) * sizeof(double));
   const size_t bb = align_up((size_t)b * b * sizeof(double));
-  const size_t ab = align_up((size_t)(a > 0 ? a : 1) * b * sizeof(double));
-  const int m = b > a ? b : a;
-  const size_t wl = align_up((size_t)leaves_of(m) * LEAF * LEAF * sizeof(double));
-  const size_t aa = align_up((size_t)(a > 0 ? a * a : 1) * sizeof(double) * 2);
+  const size_t ta = align_up((size_t)(a > 0 ? a : 1) * b * sizeof(double));
+  const size_t tmp = align_up((size_t)(n + 1) * ntm * 128 * 128 * sizeof(double));
   if (o) {
-    o->W = reinterpret_cast<double*>(base);
-    o->T1 = reinterpret_cast<double*>(base + bb);
-    o->tmp = reinterpret_cast<double*>(base + 2 * bb);
-    o->T2 = reinterpret_cast<double*>(base + 3 * bb);
-    o->winv = reinterpret_cast<double*>(base + 3 * bb + ab);
-    o->Wt = reinterpret_cast<double*>(base + 3 * bb + ab + wl);
+    o->Wall = reinterpret_cast<double*>(base);
+    o->Wt = reinterpret_cast<double*>(base + wall);
+    o->T1 = reinterpret_cast<double*>(base + wall + wt);
+    o->T3 = reinterpret_cast<double*>(base + wall + wt + bb);
+    o->Ta = reinterpret_cast<double*>(base + wall + wt + 2 * bb);
+    o->tmp = reinterpret_cast<double*>(base + wall + wt + 2 * bb + ta);
   }
-  return 3 * bb + ab + wl + aa;
+  return wall + wt + 2 * bb + ta + tmp;
 }
 
-static int gemm(cudaStream_t st, bool ta, bool tb, double* C, long long ldc, const double* A,
-                long long lda, const double* B, long long ldb, int M, int N, int K, double alpha,
-                double beta, int a_tri, int b_tri) {
-  GemmArgs g{};
-  g.A = seg1(const_cast<double*>(A), lda);
-  g.B = seg1(const_cast<double*>(B), ldb);
-  g.C = seg1(C, ldc);
-  g.M = M; g.N = N; g.K = K;
-  g.alpha = alpha; g.beta = beta;
-  g.a_tri = a_tri; g.b_tri = b_tri;
-  g.batch = 1;
-  return gemm_launch(g, ta, tb, st);
+static int launch_job(const TileJob& j, cudaStream_t st) {
+  const int tm = (j.M + 127) / 128, tn = (j.N + 127) / 128;
+  const int tiles = j.lower ? tm * (tm + 1) / 2 : tm * tn;
+  if (tiles <= 0) return 0;
+  tile_job_kernel<<<tiles, SI_NT, SI_SMEM_DOUBLES * sizeof(double), st>>>(j, tn);
+  count_launch();
+  return (int)cudaGetLastError();
+}
+
+static Prod prod(const double* A, long long lda, int akm, const double* B, long long ldb, int bkm,
+                 int K, double sgn, int ktri = 0) {
+  Prod p{};
+  p.A = A; p.lda = lda; p.akm = akm;
+  p.B = B; p.ldb = ldb; p.bkm = bkm;
+  p.K = K; p.sgn = sgn; p.ktri = ktri;
+  p.arows_all = 0;
+  return p;
+}
+
+static TileJob job(double* C, long long ldc, int M, int N, double alpha) {
+  TileJob j{};
+  j.C = C; j.ldc = ldc; j.M = M; j.N = N; j.alpha = alpha;
+  return j;
 }
 
 }  // namespace stbta
@@ -95,59 +313,87 @@ int stbta_pobtasi(const double* factor, double* inv, int n, int b, int a, int ha
   double* Xa = Xl + (n - 1) * bb;
   double* Xt = Xa + (long long)n * a * b;
   const bool arrow = has_arrow && a > 0;
-  DenseCtx c{st, nullptr, ws.winv, nullptr};
-  int e = (int)cudaMemsetAsync(inv, 0, stbta_storage_elems(n, b, a) * sizeof(double), st);
-  if (e) return e;
-
-  if (a > 0) {  // X_tip = W_t^T W_t
-    double* Wt = ws.Wt;
-    if ((e = trtri_rec(c, Lt, a, Wt, a, a, ws.tmp, 0))) return e;
-    if ((e = gemm(st, true, false, Xt, a, Wt, a, Wt, a, a, a, a, 1.0, 0.0, TRI_UPPER, TRI_LOWER)))
-      return e;
+  const size_t smem = SI_SMEM_DOUBLES * sizeof(double);
+  static bool attr = false;
+  int e;
+  if (!attr) {
+    if ((e = (int)cudaFuncSetAttribute(tile_job_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))) return e;
+    if ((e = (int)cudaFuncSetAttribute(inv_diag_tiles_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))) return e;
+    if ((e = (int)cudaFuncSetAttribute(inv_offdiag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))) return e;
+    attr = true;
   }
-  const dim3 tgrid(ceil_div(b, 32), ceil_div(b, 32)), tblk(32, 8);
-  for (int i = n - 1; i >= 0; --i) {
-    const double* Lii = Ld + i * bb;
-    const double* sub = (i < n - 1) ? Ll + i * bb : nullptr;
-    const double* arr = arrow ? La + (long long)i * a * b : nullptr;
-    if ((e = trtri_rec(c, Lii, b, ws.W, b, b, ws.tmp, 0))) return e;
-    if (sub) {
-      // T1 = X_{i+1,i+1} L_{i+1,i} (+ X_{a,i+1}^T L_{a,i});  X_{i+1,i} = -T1 W
-      if ((e = gemm(st, false, false, ws.T1, b, Xd + (i + 1) * bb, b, sub, b, b, b, b, 1.0, 0.0,
-                    TRI_NONE, TRI_NONE)))
-        return e;
-      if (arr && (e = gemm(st, true, false, ws.T1, b, Xa + (long long)(i + 1) * a * b, b, arr, b,
-                           b, b, a, 1.0, 1.0, TRI_NONE, TRI_NONE)))
-        return e;
-      if ((e = gemm(st, false, false, Xl + i * bb, b, ws.T1, b, ws.W, b, b, b, b, -1.0, 0.0,
-                    TRI_NONE, TRI_LOWER)))
-        return e;
-    }
-    if (arr) {
-      // T2 = X_tip L_{a,i} (+ X_{a,i+1} L_{i+1,i});  X_{a,i} = -T2 W
-      if ((e = gemm(st, false, false, ws.T2, b, Xt, a, arr, b, a, b, a, 1.0, 0.0, TRI_NONE,
-                    TRI_NONE)))
-        return e;
-      if (sub && (e = gemm(st, false, false, ws.T2, b, Xa + (long long)(i + 1) * a * b, b, sub, b,
-                           a, b, b, 1.0, 1.0, TRI_NONE, TRI_NONE)))
-        return e;
-      if ((e = gemm(st, false, false, Xa + (long long)i * a * b, b, ws.T2, b, ws.W, b, a, b, b,
-                    -1.0, 0.0, TRI_NONE, TRI_LOWER)))
-        return e;
-    }
-    // T1 = W^T - X_{i+1,i}^T L_{i+1,i} - X_{a,i}^T L_{a,i};  X_ii = T1 W
-    transpose_kernel<<<tgrid, tblk, 0, st>>>(ws.W, b, ws.T1, b, b, nullptr);
+
+  // ---- 1. all inverses W_i (and W_tip) up front
+  InvSet s{};
+  s.L = Ld; s.W = ws.Wall; s.Lt = Lt; s.Wt = ws.Wt;
+  s.n = n; s.b = b; s.a = a; s.tmp = ws.tmp;
+  s.ntb = (b + 127) / 128;
+  const int nta = a > 0 ? (a + 127) / 128 : 0;
+  const int nm = n + (a > 0 ? 1 : 0);
+  const int ntm = s.ntb > nta ? s.ntb : nta;
+  if (a > 0 && (e = (int)cudaMemsetAsync(ws.Wt, 0, (size_t)a * a * sizeof(double), st))) return e;
+  inv_diag_tiles_kernel<<<dim3(ntm, nm), SI_NT, smem, st>>>(s);
+  count_launch();
+  if ((e = (int)cudaGetLastError())) return e;
+  for (int d = 1; d < ntm; ++d) {
+    inv_offdiag_kernel<<<dim3(ntm - d, nm), SI_NT, smem, st>>>(s, d);
     count_launch();
     if ((e = (int)cudaGetLastError())) return e;
-    if (sub && (e = gemm(st, true, false, ws.T1, b, Xl + i * bb, b, sub, b, b, b, b, -1.0, 1.0,
-                         TRI_NONE, TRI_NONE)))
-      return e;
-    if (arr && (e = gemm(st, true, false, ws.T1, b, Xa + (long long)i * a * b, b, arr, b, b, b, a,
-                         -1.0, 1.0, TRI_NONE, TRI_NONE)))
-      return e;
-    if ((e = gemm(st, false, false, Xd + i * bb, b, ws.T1, b, ws.W, b, b, b, b, 1.0, 0.0, TRI_NONE,
-                  TRI_LOWER)))
-      return e;
+  }
+
+  // ---- 2. X_tip = W_t^T W_t ;  X_a = 0 when the arrow is inactive
+  if (a > 0) {
+    TileJob j = job(Xt, a, a, a, 1.0);
+    j.nprod = 1;
+    j.p[0] = prod(ws.Wt, a, 1, ws.Wt, a, 1, a, 1.0);
+    if ((e = launch_job(j, st))) return e;
+    if (!arrow && (e = (int)cudaMemsetAsync(Xa, 0, (size_t)n * a * b * sizeof(double), st))) return e;
+  }
+
+  // ---- 3. the recursion, i = n-1 .. 0
+  for (int i = n - 1; i >= 0; --i) {
+    const double* W = ws.Wall + i * bb;
+    const double* sub = (i < n - 1) ? Ll + i * bb : nullptr;
+    const double* arr = arrow ? La + (long long)i * a * b : nullptr;
+    if (sub) {
+      // T1 = X_{i+1,i+1} L_{i+1,i} (+ X_{a,i+1}^T L_{a,i})
+      TileJob j = job(ws.T1, b, b, b, 1.0);
+      j.p[j.nprod++] = prod(Xd + (i + 1) * bb, b, 0, sub, b, 1, b, 1.0);
+      if (arr) j.p[j.nprod++] = prod(Xa + (long long)(i + 1) * a * b, b, 1, arr, b, 1, a, 1.0);
+      if ((e = launch_job(j, st))) return e;
+      // X_{i+1,i} = -T1 W
+      TileJob j2 = job(Xl + i * bb, b, b, b, -1.0);
+      j2.p[j2.nprod++] = prod(ws.T1, b, 0, W, b, 1, b, 1.0, 1);
+      if ((e = launch_job(j2, st))) return e;
+    }
+    if (arr) {
+      // Ta = X_tip L_{a,i} (+ X_{a,i+1} L_{i+1,i});  X_{a,i} = -Ta W
+      TileJob j = job(ws.Ta, b, a, b, 1.0);
+      j.p[j.nprod++] = prod(Xt, a, 0, arr, b, 1, a, 1.0);
+      if (sub) j.p[j.nprod++] = prod(Xa + (long long)(i + 1) * a * b, b, 0, sub, b, 1, b, 1.0);
+      if ((e = launch_job(j, st))) return e;
+      TileJob j2 = job(Xa + (long long)i * a * b, b, a, b, -1.0);
+      j2.p[j2.nprod++] = prod(ws.Ta, b, 0, W, b, 1, b, 1.0, 1);
+      if ((e = launch_job(j2, st))) return e;
+    }
+    // T3 = W^T - X_{i+1,i}^T L_{i+1,i} - X_{a,i}^T L_{a,i}
+    {
+      TileJob j = job(ws.T3, b, b, b, 1.0);
+      j.init = 2;
+      j.ci = W;
+      j.ldci = b;
+      if (sub) j.p[j.nprod++] = prod(Xl + i * bb, b, 1, sub, b, 1, b, -1.0);
+      if (arr) j.p[j.nprod++] = prod(Xa + (long long)i * a * b, b, 1, arr, b, 1, a, -1.0);
+      if ((e = launch_job(j, st))) return e;
+    }
+    // X_ii = T3 W  (lower tiles, mirrored)
+    {
+      TileJob j = job(Xd + i * bb, b, b, b, 1.0);
+      j.lower = 1;
+      j.mirror = 1;
+      j.p[j.nprod++] = prod(ws.T3, b, 0, W, b, 1, b, 1.0, 1);
+      if ((e = launch_job(j, st))) return e;
+    }
   }
   return 0;
 }

@@ -299,4 +299,81 @@ STBTA_DEV void trsm_strip_smem(double* X, const double* Ls, const double* WT, in
   }
 }
 
+// ---------------------------------------------------------------------------
+// In-CTA inversion of a factored lower 128x128 tile (identity-padded) held in
+// smem[0 .. 128*INV_LD): W = L^-1.  Warp kb inverts the 32x32 diagonal block
+// kb (one column per lane); the off-diagonal blocks follow by diagonals,
+// W_ij = -W_ii sum_{k=j}^{i-1} L_ik W_kj (SIMT 32x32 block products).
+// Layout after return: L lower unchanged, W_ij^T (i > j) in the upper block
+// (j, i), W_kk row-major in the Wd area.  Read with inv_tile_at().
+constexpr int INV_LD = 129, BLD = 33;
+constexpr int INV_SMEM_DOUBLES = 128 * INV_LD + 11 * 32 * BLD;
+
+template <int NT>
+STBTA_DEV void invert_tile_smem(double* sm) {
+  double* T = sm;
+  double* WT = T + 128 * INV_LD;   // W_kk^T: WT[kb][c][i] = W_kk[i][c]
+  double* Wd = WT + 4 * 32 * BLD;  // W_kk row-major
+  double* TS = Wd + 4 * 32 * BLD;  // scratch products, 3 blocks
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (warp < 4) {
+    const int k0 = warp * 32;
+    double* dinv = TS + warp * 32;
+    dinv[lane] = 1.0 / T[(k0 + lane) * INV_LD + k0 + lane];
+    __syncwarp();
+    double w[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) w[i] = (i == lane) ? 1.0 : 0.0;
+#pragma unroll 32
+    for (int k = 0; k < 32; ++k) {
+      w[k] *= dinv[k];
+#pragma unroll 32
+      for (int i = k + 1; i < 32; ++i) w[i] = fma(-T[(k0 + i) * INV_LD + k0 + k], w[k], w[i]);
+    }
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      WT[warp * 32 * BLD + lane * BLD + i] = w[i];
+      Wd[warp * 32 * BLD + i * BLD + lane] = w[i];
+    }
+  }
+  __syncthreads();
+  for (int d = 1; d < 4; ++d) {
+    const int nb = 4 - d, blk = tid >> 6, id = tid & 63, tr = id & 7, tc = id >> 3;
+    if (blk < nb) {  // T_j = sum_k L_ik W_kj  (i = j + d)
+      const int j = blk, i = j + d;
+      double acc[4][4];
+      zero4x4(acc);
+      for (int k = j; k < i; ++k) {
+        const double* b = (k == j) ? WT + j * 32 * BLD : T + (32 * j) * INV_LD + 32 * k;
+        const int ldb = (k == j) ? BLD : INV_LD;
+        mma32_blk<32, true>(acc, T + (32 * i) * INV_LD + 32 * k, INV_LD, b, ldb, id);
+      }
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) TS[j * 32 * BLD + (tr + 8 * a) * BLD + tc + 8 * c] = acc[a][c];
+    }
+    __syncthreads();
+    if (blk < nb) {  // W_ij = -W_ii T_j, stored transposed into T's upper block (j, i)
+      const int j = blk, i = j + d;
+      double acc[4][4];
+      zero4x4(acc);
+      mma32_blk<32, false>(acc, Wd + i * 32 * BLD, BLD, TS + j * 32 * BLD, BLD, id);
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          T[(32 * j + tc + 8 * c) * INV_LD + 32 * i + tr + 8 * a] = -acc[a][c];
+    }
+    __syncthreads();
+  }
+}
+
+STBTA_DEV double inv_tile_at(const double* sm, int r, int c) {
+  if (c > r) return 0.0;
+  const double* Wd = sm + 128 * INV_LD + 4 * 32 * BLD;
+  if ((r >> 5) == (c >> 5)) return Wd[(r >> 5) * 32 * BLD + (r & 31) * BLD + (c & 31)];
+  return sm[c * INV_LD + r];
+}
+
 }  // namespace stbta

@@ -28,9 +28,44 @@ struct MmaCfg {
   static_assert(WARPS_M * WARPS_N * 32 == NT, "warp layout must cover the CTA");
   static constexpr int MF = WM / 8, NF = WN / 8;
   static constexpr int BK = BK_, STAGES = ST_, LDS = BK + 4;
-  static constexpr int A_STAGE = BM * LDS, B_STAGE = BN * LDS;
+  // [k][m] (k-major) staging of an operand stored K x M in memory
+  static constexpr int LDA_KM = BM + 4, LDB_KM = BN + 4;
+  static constexpr int A_STAGE = (BM * LDS > BK * LDA_KM ? BM * LDS : BK * LDA_KM);
+  static constexpr int B_STAGE = (BN * LDS > BK * LDB_KM ? BN * LDS : BK * LDB_KM);
   static constexpr int SMEM_DOUBLES = STAGES * (A_STAGE + B_STAGE);
 };
+
+// Slab of an operand stored k-major (element (row, k) at p[k * ld + row]):
+// BK k-rows x ROWS columns into sm[k][row] with row stride ROWS + 4.
+template <int ROWS, int NT, int BK>
+STBTA_DEV void load_slab_km(double* sm, const Opnd& o, int k0, int K) {
+  constexpr int LD = ROWS + 4;
+  const int tid = threadIdx.x;
+  if (o.vec) {
+    constexpr int PAIRS = BK * ROWS / 2;
+#pragma unroll
+    for (int e = tid; e < PAIRS; e += NT) {
+      const int k = e / (ROWS / 2), c = (e % (ROWS / 2)) * 2;
+      const int gk = k0 + k;
+      int bytes = 0;
+      const double* src = o.p;
+      if (gk < K && c < o.rows) {
+        bytes = (c + 1 < o.rows) ? 16 : 8;
+        src = o.p + (long long)gk * o.ld + c;
+      }
+      cp_async16(sm + k * LD + c, src, bytes);
+    }
+  } else {
+    constexpr int ELEMS = BK * ROWS;
+#pragma unroll
+    for (int e = tid; e < ELEMS; e += NT) {
+      const int k = e / ROWS, c = e % ROWS;
+      const int gk = k0 + k;
+      const bool ok = gk < K && c < o.rows;
+      cp_async8(sm + k * LD + c, ok ? o.p + (long long)gk * o.ld + c : o.p, ok);
+    }
+  }
+}
 
 template <int ROWS, int NT, int BK = 16>
 STBTA_DEV void load_slab(double* sm, const Opnd& o, int k0, int K) {
@@ -67,9 +102,9 @@ STBTA_DEV void load_slab(double* sm, const Opnd& o, int k0, int K) {
 // column is >= n_active skip the arithmetic (triangular strips).  All threads
 // of the CTA must call; smem holds Cfg::SMEM_DOUBLES doubles.  Ends with a
 // __syncthreads so the caller may reuse shared memory.
-template <class Cfg, bool NEG = false, int DBG = 0>
+template <class Cfg, bool NEG = false, int DBG = 0, bool AKM = false, bool BKM = false>
 STBTA_DEV void tile_mma(double (&acc)[Cfg::MF][Cfg::NF][2], const Opnd& A, const Opnd& B, int K,
-                        int n_active, double* smem) {
+                        int n_active, double* smem, int kbeg = 0) {
   constexpr int MF = Cfg::MF, NF = Cfg::NF, BK = Cfg::BK, ST = Cfg::STAGES, LDS = Cfg::LDS;
   double* As = smem;
   double* Bs = smem + ST * Cfg::A_STAGE;
@@ -78,14 +113,17 @@ STBTA_DEV void tile_mma(double (&acc)[Cfg::MF][Cfg::NF][2], const Opnd& A, const
   const int wm0 = (warp % Cfg::WARPS_M) * Cfg::WM;
   const int wn0 = (warp / Cfg::WARPS_M) * Cfg::WN;
   const bool active = wn0 < n_active;
-  const int ktiles = (K + BK - 1) / BK;
+  const int ktiles = (K - kbeg + BK - 1) / BK;
+  auto load_stage = [&](int slot, int k0) {
+    if (AKM) load_slab_km<Cfg::BM, Cfg::NT, Cfg::BK>(As + slot * Cfg::A_STAGE, A, k0, K);
+    else load_slab<Cfg::BM, Cfg::NT, Cfg::BK>(As + slot * Cfg::A_STAGE, A, k0, K);
+    if (BKM) load_slab_km<Cfg::BN, Cfg::NT, Cfg::BK>(Bs + slot * Cfg::B_STAGE, B, k0, K);
+    else load_slab<Cfg::BN, Cfg::NT, Cfg::BK>(Bs + slot * Cfg::B_STAGE, B, k0, K);
+  };
 
 #pragma unroll
   for (int s = 0; s < ST - 1; ++s) {
-    if (s < ktiles) {
-      load_slab<Cfg::BM, Cfg::NT, Cfg::BK>(As + s * Cfg::A_STAGE, A, s * BK, K);
-      load_slab<Cfg::BN, Cfg::NT, Cfg::BK>(Bs + s * Cfg::B_STAGE, B, s * BK, K);
-    }
+    if (s < ktiles) load_stage(s, kbeg + s * BK);
     cp_async_commit();
   }
   for (int kt = 0; kt < ktiles; ++kt) {
@@ -94,10 +132,7 @@ STBTA_DEV void tile_mma(double (&acc)[Cfg::MF][Cfg::NF][2], const Opnd& A, const
       __syncthreads();
     }
     const int nt = kt + ST - 1;
-    if (DBG != 2 && nt < ktiles) {  // DBG 2: no loads in the main loop
-      load_slab<Cfg::BM, Cfg::NT, Cfg::BK>(As + (nt % ST) * Cfg::A_STAGE, A, nt * BK, K);
-      load_slab<Cfg::BN, Cfg::NT, Cfg::BK>(Bs + (nt % ST) * Cfg::B_STAGE, B, nt * BK, K);
-    }
+    if (DBG != 2 && nt < ktiles) load_stage(nt % ST, kbeg + nt * BK);  // DBG 2: no loads
     cp_async_commit();
     if (active) {
       const double* as = As + (kt % ST) * Cfg::A_STAGE;
@@ -107,9 +142,14 @@ STBTA_DEV void tile_mma(double (&acc)[Cfg::MF][Cfg::NF][2], const Opnd& A, const
         const int k = ks * 4 + tq;
         double af[MF], bf[NF];
 #pragma unroll
-        for (int i = 0; i < MF; ++i) af[i] = as[(wm0 + i * 8 + gq) * LDS + k];
+        for (int i = 0; i < MF; ++i)
+          af[i] = AKM ? as[k * Cfg::LDA_KM + wm0 + i * 8 + gq] : as[(wm0 + i * 8 + gq) * LDS + k];
 #pragma unroll
-        for (int j = 0; j < NF; ++j) bf[j] = NEG ? -bs[(wn0 + j * 8 + gq) * LDS + k] : bs[(wn0 + j * 8 + gq) * LDS + k];
+        for (int j = 0; j < NF; ++j) {
+          const double bv =
+              BKM ? bs[k * Cfg::LDB_KM + wn0 + j * 8 + gq] : bs[(wn0 + j * 8 + gq) * LDS + k];
+          bf[j] = NEG ? -bv : bv;
+        }
 #pragma unroll
         for (int i = 0; i < MF; ++i)
 #pragma unroll
