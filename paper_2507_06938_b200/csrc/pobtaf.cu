@@ -37,7 +37,7 @@ namespace stbta {
 constexpr int DAG_NT = 256;
 using Cfg128 = MmaCfg<128, 128, 64, 32, DAG_NT>;
 using Cfg32 = MmaCfg<32, 128, 32, 16, DAG_NT>;
-constexpr int TRSM_SMEM_DOUBLES = 32 * 132 + 128 * PT_LD + 4 * 32 * PT_WLD;
+constexpr int TRSM_SMEM_DOUBLES = 32 * 132 + 128 * 132 + 4 * 32 * PT_WLD;
 constexpr int cmax(int x, int y) { return x > y ? x : y; }
 constexpr int DAG_SMEM_DOUBLES =
     cmax(cmax(PT_SMEM_DOUBLES, TRSM_SMEM_DOUBLES), Cfg128::SMEM_DOUBLES);
@@ -129,12 +129,24 @@ struct Task {
   int type, s, R, C, q;
 };
 
-STBTA_DEV Task decode(const Band& g, const DagWs& ws, int t) {
-  int lo = 0, hi = ws.G;  // gstart[lo] <= t < gstart[hi]
+// Group containing ticket t (gstart[lo] <= t < gstart[lo+1]): a 32-ary search
+// by one full warp (3 dependent load rounds instead of ~13 for a binary search).
+STBTA_DEV int find_group(const DagWs& ws, int t) {
+  const int lane = threadIdx.x & 31;
+  int lo = 0, hi = ws.G;  // invariant: gstart[lo] <= t < gstart[hi]
   while (hi - lo > 1) {
-    const int mid = (lo + hi) >> 1;
-    if (__ldg(ws.gstart + mid) <= t) lo = mid; else hi = mid;
+    const int step = (hi - lo + 31) / 32;
+    const int idx = lo + (lane + 1) * step;
+    const bool le = idx < hi && __ldg(ws.gstart + idx) <= t;
+    const int cnt = __popc(__ballot_sync(0xffffffffu, le));
+    const int nlo = lo + cnt * step;
+    hi = min(hi, nlo + step);
+    lo = nlo;
   }
+  return lo;
+}
+
+STBTA_DEV Task decode(const Band& g, const DagWs& ws, int t, int lo) {
   const int kind = lo % NGRP, s = lo / NGRP;
   int local = t - __ldg(ws.gstart + lo);
   Task k{};
@@ -285,11 +297,17 @@ __global__ void __launch_bounds__(DAG_NT, 1) pobtaf_dag_kernel(Band g, DagWs ws,
   }
 
   for (;;) {
-    if (tid == 0) {
-      const int t = atomicAdd(ws.ticket, 1);
-      s_ticket = t;
-      if (t < total) s_task = decode(g, ws, t);
-      s_ok = 1;
+    if (tid < 32) {
+      int t = 0;
+      if (tid == 0) t = atomicAdd(ws.ticket, 1);
+      t = __shfl_sync(0xffffffffu, t, 0);
+      int grp = 0;
+      if (t < total) grp = find_group(ws, t);
+      if (tid == 0) {
+        s_ticket = t;
+        if (t < total) s_task = decode(g, ws, t, grp);
+        s_ok = 1;
+      }
     }
     __syncthreads();
     if (s_ticket >= total) break;
@@ -328,8 +346,9 @@ __global__ void __launch_bounds__(DAG_NT, 1) pobtaf_dag_kernel(Band g, DagWs ws,
       if (rows > 0) {
         constexpr int XLD = 132;
         double* X = smem;                 // 32 x XLD
-        double* Ls = X + 32 * XLD;        // 128 x PT_LD (strictly lower blocks used)
-        double* WT = Ls + 128 * PT_LD;    // 4 x 32 x PT_WLD
+        constexpr int TLD = 132;          // 4 mod 16: conflict-free fragment reads
+        double* Ls = X + 32 * XLD;        // 128 x TLD (strictly lower blocks used)
+        double* WT = Ls + 128 * TLD;      // 4 x 32 x PT_WLD
         const TilePtr xp = tile_ptr(g, tk.R, s);
         const TilePtr lp = tile_ptr(g, s, s);
         double* Xg = xp.p + (long long)r0 * xp.ld;
@@ -341,8 +360,8 @@ __global__ void __launch_bounds__(DAG_NT, 1) pobtaf_dag_kernel(Band g, DagWs ws,
         for (int e = tid; e < 128 * 128; e += DAG_NT) {
           const int r = e >> 7, c = e & 127;
           if ((r >> 5) > (c >> 5)) {  // strictly-lower 32-blocks
-            if (r < w && c < w) cp_async8(Ls + r * PT_LD + c, lp.p + (long long)r * lp.ld + c, true);
-            else Ls[r * PT_LD + c] = 0.0;
+            if (r < w && c < w) cp_async8(Ls + r * TLD + c, lp.p + (long long)r * lp.ld + c, true);
+            else Ls[r * TLD + c] = 0.0;
           }
         }
         const double* Wg = ws.W + (long long)s * W_SLOT;
@@ -353,7 +372,7 @@ __global__ void __launch_bounds__(DAG_NT, 1) pobtaf_dag_kernel(Band g, DagWs ws,
         cp_async_commit();
         cp_async_wait<0>();
         __syncthreads();
-        trsm_strip_smem<DAG_NT, XLD>(X, Ls, WT, w);
+        trsm_strip_smem<DAG_NT, XLD, TLD>(X, Ls, WT, w);
         for (int e = tid; e < rows * w; e += DAG_NT) {
           const int r = e / w, c = e - r * w;
           Xg[(long long)r * xp.ld + c] = X[r * XLD + c];

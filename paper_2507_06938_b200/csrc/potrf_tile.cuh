@@ -239,7 +239,7 @@ STBTA_DEV int potrf_tile_smem(double* T, double* WT, double* scratch, double* lo
 // with L's strictly-lower 32-blocks in Ls (ld PT_LD) and the diagonal block
 // inverses as WT[kb][c][i] = W_kk[i][c] (ld PT_WLD).  Right-looking over the
 // 32-column blocks; zero rows stay zero.
-template <int NT, int XLD>
+template <int NT, int XLD, int LLD = PT_LD>
 STBTA_DEV void trsm_strip_smem(double* X, const double* Ls, const double* WT, int w) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
@@ -285,7 +285,7 @@ STBTA_DEV void trsm_strip_smem(double* X, const double* Ls, const double* WT, in
         if (tix < njb * 16) cnt = u + 1;
       }
       // B(k, n) = L[n][kb*32 + k]
-      frags_mma<U>(c0, c1, X + kb * 32, XLD, Ls + kb * 32, PT_LD, true, mt, nt, cnt, 32);
+      frags_mma<U>(c0, c1, X + kb * 32, XLD, Ls + kb * 32, LLD, true, mt, nt, cnt, 32);
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         if (u < cnt) {

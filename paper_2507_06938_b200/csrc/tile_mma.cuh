@@ -178,16 +178,26 @@ STBTA_DEV void acc_load(double (&acc)[Cfg::MF][Cfg::NF][2], const double* C, lon
   const int gq = lane >> 2, tq = lane & 3;
   const int wm0 = (warp % Cfg::WARPS_M) * Cfg::WM;
   const int wn0 = (warp / Cfg::WARPS_M) * Cfg::WN;
+  const bool vec = ((uintptr_t)C % 16 == 0) && (ldc % 2 == 0);
 #pragma unroll
   for (int i = 0; i < Cfg::MF; ++i) {
     const int m = wm0 + i * 8 + gq;
 #pragma unroll
     for (int j = 0; j < Cfg::NF; ++j) {
+      const int n0 = wn0 + j * 8 + 2 * tq;
+      const double* src = C + (long long)m * ldc + n0;
+      const bool full = vec && m < rows && n0 + 1 < cols && !(lower && n0 + 1 > m + diag);
+      if (full) {
+        const double2 v = __ldcg(reinterpret_cast<const double2*>(src));
+        acc[i][j][0] = v.x;
+        acc[i][j][1] = v.y;
+      } else {
 #pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int nn = wn0 + j * 8 + 2 * tq + e;
-        const bool ok = m < rows && nn < cols && !(lower && nn > m + diag);
-        acc[i][j][e] = ok ? __ldcg(C + (long long)m * ldc + nn) : 0.0;
+        for (int e = 0; e < 2; ++e) {
+          const int nn = n0 + e;
+          const bool ok = m < rows && nn < cols && !(lower && nn > m + diag);
+          acc[i][j][e] = ok ? __ldcg(src + e) : 0.0;
+        }
       }
     }
   }
@@ -202,6 +212,7 @@ STBTA_DEV void acc_store(const double (&acc)[Cfg::MF][Cfg::NF][2], double* C, lo
   const int gq = lane >> 2, tq = lane & 3;
   const int wm0 = (warp % Cfg::WARPS_M) * Cfg::WM;
   const int wn0 = (warp / Cfg::WARPS_M) * Cfg::WN;
+  const bool vec = ((uintptr_t)C % 16 == 0) && (ldc % 2 == 0);
 #pragma unroll
   for (int i = 0; i < Cfg::MF; ++i) {
     const int m = wm0 + i * 8 + gq;
@@ -209,9 +220,14 @@ STBTA_DEV void acc_store(const double (&acc)[Cfg::MF][Cfg::NF][2], double* C, lo
     double* crow = C + (long long)m * ldc;
 #pragma unroll
     for (int j = 0; j < Cfg::NF; ++j) {
+      const int n0 = wn0 + j * 8 + 2 * tq;
+      if (vec && !op && n0 + 1 < cols && !(lower && n0 + 1 > m + diag)) {
+        *reinterpret_cast<double2*>(crow + n0) = make_double2(alpha * acc[i][j][0], alpha * acc[i][j][1]);
+        continue;
+      }
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
-        const int nn = wn0 + j * 8 + 2 * tq + e;
+        const int nn = n0 + e;
         if (nn >= cols || (lower && nn > m + diag)) continue;
         double v = alpha * acc[i][j][e];
         if (op) v += __ldcg(crow + nn);
