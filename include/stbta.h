@@ -49,6 +49,17 @@ size_t stbta_pobtaf_workspace_bytes(int n, int b, int a);
 int stbta_pobtaf(double* data, int n, int b, int a, int use_arrow, double* logdet_out, int* info,
                  void* workspace, size_t workspace_bytes, void* stream);
 
+/* Region-pointer form of POBTAF (diag (n,b,b), lower (n-1,b,b), arrow (n,a,b),
+ * tip (a,a) may live in separate buffers) with a partial-elimination count:
+ * nfact < 0 is the full factorization; 0 <= nfact <= n factorizes only the
+ * first nfact time blocks, leaving the later blocks and the tip updated by
+ * their Schur complement but unfactored, and
+ * logdet_out covering the eliminated blocks only (time partitions of
+ * bta_dist.d_factorize, reference bta_dist.py:174-254). */
+int stbta_pobtaf_ex(double* diag, double* lower, double* arrow, double* tip, int n, int b, int a,
+                    int use_arrow, int nfact, double* logdet_out, int* info, void* workspace,
+                    size_t workspace_bytes, void* stream);
+
 /* ---------------------------------------------------------------- POBTAS --
  * Triangular solves against a POBTAF factor, in place on rhs (dim x nrhs,
  * row-major, dim = n*b+a).  mode 0: L L^T x = r (bta.solve, bta.py:305-307);
@@ -58,6 +69,11 @@ size_t stbta_pobtas_workspace_bytes(int n, int b, int a, int nrhs);
 int stbta_pobtas(const double* factor, int n, int b, int a, int has_arrow, double* rhs, int nrhs,
                  int mode, void* workspace, size_t workspace_bytes, void* stream);
 
+/* Region-pointer form of POBTAS. */
+int stbta_pobtas_ex(const double* diag, const double* lower, const double* arrow,
+                    const double* tip, int n, int b, int a, int has_arrow, double* rhs, int nrhs,
+                    int mode, void* workspace, size_t workspace_bytes, void* stream);
+
 /* --------------------------------------------------------------- POBTASI --
  * Selected inversion: the BTA-pattern entries of (L L^T)^-1 written to `inv`
  * (a separate buffer of the same layout; X_ii stored full symmetric).
@@ -65,6 +81,15 @@ int stbta_pobtas(const double* factor, int n, int b, int a, int has_arrow, doubl
 size_t stbta_pobtasi_workspace_bytes(int n, int b, int a);
 int stbta_pobtasi(const double* factor, double* inv, int n, int b, int a, int has_arrow,
                   void* workspace, size_t workspace_bytes, void* stream);
+
+/* Region-pointer form of POBTASI.  nstart < 0 is the full selected inversion;
+ * 0 <= nstart <= n continues a recursion whose blocks nstart.. (X diag /
+ * lower / arrow) and X_tip are already in the output
+ * (partition interiors of bta_dist.d_selected_invert, bta_dist.py:461-602). */
+int stbta_pobtasi_ex(const double* Ld, const double* Ll, const double* La, const double* Lt,
+                     double* Xd, double* Xl, double* Xa, double* Xt, int n, int b, int a,
+                     int has_arrow, int nstart, void* workspace, size_t workspace_bytes,
+                     void* stream);
 
 /* ------------------------------------------------------ Q assembly / f_obj --
  * stbta_assemble: write the theta-dependent values of a precision matrix into

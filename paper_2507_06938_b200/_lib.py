@@ -30,6 +30,18 @@ _SIGNATURES = {
     "stbta_storage_elems": (c_ll, [c_int, c_int, c_int]),
     "stbta_pobtaf_workspace_bytes": (c_size, [c_int, c_int, c_int]),
     "stbta_pobtaf": (c_int, [c_vp, c_int, c_int, c_int, c_int, c_vp, c_vp, c_vp, c_size, c_vp]),
+    "stbta_pobtaf_ex": (
+        c_int,
+        [c_vp, c_vp, c_vp, c_vp, c_int, c_int, c_int, c_int, c_int, c_vp, c_vp, c_vp, c_size, c_vp],
+    ),
+    "stbta_pobtas_ex": (
+        c_int,
+        [c_vp, c_vp, c_vp, c_vp, c_int, c_int, c_int, c_int, c_vp, c_int, c_int, c_vp, c_size, c_vp],
+    ),
+    "stbta_pobtasi_ex": (
+        c_int,
+        [c_vp] * 8 + [c_int, c_int, c_int, c_int, c_int, c_vp, c_size, c_vp],
+    ),
     "stbta_pobtas_workspace_bytes": (c_size, [c_int, c_int, c_int, c_int]),
     "stbta_pobtas": (
         c_int,

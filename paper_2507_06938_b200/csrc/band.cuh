@@ -26,11 +26,13 @@ constexpr int TS = 32;   // strip (row sub-tile) size
 constexpr int NSTRIP = TT / TS;
 
 struct Band {
-  double* data;  // flat BTA storage
+  double* data;  // flat BTA storage (unused when the region pointers are set)
+  double *dg, *lw, *ar, *tp;  // diag (n,b,b) | lower (n-1,b,b) | arrow (n,a,b) | tip (a,a)
   int n, b, a;
   int nbt;       // tiles per time block
   int nat;       // arrow tiles
   int S;         // panels = n*nbt + nat
+  int SP;        // panels actually eliminated (S, or nfact*nbt for a partial factorization)
   int use_arrow; // arrow rows take part in the block eliminations
   int vec_b;     // b even: rows of diag/lower/arrow are 16-byte aligned
   int vec_a;     // tip rows 16-byte aligned (a even and b even)
@@ -58,10 +60,10 @@ struct TilePtr {
 STBTA_DEV TilePtr tile_ptr(const Band& g, int R, int C) {
   const long long b = g.b;
   const long long bb = b * b;
-  double* diag = g.data;
-  double* lower = diag + (long long)g.n * bb;
-  double* arrow = lower + (long long)(g.n - 1) * bb;
-  double* tip = arrow + (long long)g.n * g.a * b;
+  double* diag = g.dg;
+  double* lower = g.lw;
+  double* arrow = g.ar;
+  double* tip = g.tp;
   TilePtr t;
   const int NB = g.n * g.nbt;
   if (C >= NB) {  // tip
@@ -90,16 +92,15 @@ STBTA_DEV TilePtr tile_ptr_upper(const Band& g, int R, int C) {
   const long long b = g.b;
   const int NB = g.n * g.nbt;
   if (C >= NB) {  // tip
-    const double* tip = g.data + (long long)(2 * g.n - 1) * b * b + (long long)g.n * g.a * b;
     TilePtr p;
-    p.p = const_cast<double*>(tip) + (long long)(C - NB) * TT * g.a + (R - NB) * TT;
+    p.p = g.tp + (long long)(C - NB) * TT * g.a + (R - NB) * TT;
     p.ld = g.a;
     p.vec = g.vec_a;
     return p;
   }
   const int t = C / g.nbt, jr = R % g.nbt, jc = C % g.nbt;
   TilePtr p;
-  p.p = g.data + (long long)t * b * b + (long long)jc * TT * b + jr * TT;
+  p.p = g.dg + (long long)t * b * b + (long long)jc * TT * b + jr * TT;
   p.ld = b;
   p.vec = g.vec_b;
   return p;
@@ -158,6 +159,16 @@ STBTA_DEV int* counter(const Band& g, int* ctr, int R, int q, int C) {
 
 inline long long counter_elems(int n, int nbt, int nat, int S) {
   return (long long)n * nbt * NSTRIP * 2 * nbt + (long long)nat * NSTRIP * S;
+}
+
+// Region pointers of the reference's flat layout.
+inline void band_set_flat(Band& g, double* data) {
+  const long long bb = (long long)g.b * g.b;
+  g.data = data;
+  g.dg = data;
+  g.lw = data ? data + (long long)g.n * bb : nullptr;
+  g.ar = data ? g.lw + (long long)(g.n - 1) * bb : nullptr;
+  g.tp = data ? g.ar + (long long)g.n * g.a * g.b : nullptr;
 }
 
 // ------------------------------------------------------------- sync helpers

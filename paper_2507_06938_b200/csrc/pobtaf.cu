@@ -85,7 +85,10 @@ STBTA_DEV bool g1_active(const Band& g, int s) {
 
 STBTA_DEV int group_size(const Band& g, int kind, int s) {
   int mb;
-  const int m = band_rows(g, s, &mb);
+  if (s >= g.SP) {  // trailing groups: only the last eliminated panel's bulk (G1, G3)
+    if (kind != 1 && kind != 3) return 0;
+  }
+  const int m = s < g.S ? band_rows(g, s, &mb) : 0;
   switch (kind) {
     case 0: return m >= 1 ? NSTRIP : 0;
     case 1: return g1_active(g, s) ? NSTRIP : 0;
@@ -101,7 +104,8 @@ STBTA_DEV int group_size(const Band& g, int kind, int s) {
   }
 }
 
-inline int n_groups(int S) { return NGRP * S; }
+// one extra (partial) group set after the last eliminated panel carries its bulk updates
+inline int n_groups(int SP) { return NGRP * SP + 4; }
 
 // one CTA of 1024 threads: gstart[gi] = sum of sizes of groups < gi
 __global__ void __launch_bounds__(1024) dag_setup_kernel(Band g, DagWs ws) {
@@ -201,7 +205,7 @@ STBTA_DEV bool potrf_worker(const Band& g, const DagWs& ws, int* info, double* s
   __shared__ double s_logdet;
   const int tid = threadIdx.x;
   const int NB = g.n * g.nbt;
-  for (int s = 0; s < g.S; ++s) {
+  for (int s = 0; s < g.SP; ++s) {
     const int w = tile_extent(g, s);
     unsigned long long t0 = 0, t1 = 0;
     if (ws.prof != nullptr && tid == 0) t0 = gtimer();
@@ -457,23 +461,36 @@ __global__ void dag_logdet_kernel(const double* slots, int count, double* out) {
 
 static size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 
-static Band make_band(double* data, int n, int b, int a, int use_arrow) {
+static bool al16(const void* p) { return ((uintptr_t)p % 16) == 0; }
+
+// nfact < 0: full factorization (all blocks and the tip).  0 <= nfact <= n:
+// factorize only the first nfact time blocks (partial elimination); the
+// remaining blocks and the tip receive their updates but stay unfactored.
+static Band make_band(const double* const* regions, int n, int b, int a, int use_arrow,
+                      int nfact) {
   Band g{};
-  g.data = data;
   g.n = n; g.b = b; g.a = a;
   g.nbt = (b + TT - 1) / TT;
   g.nat = a > 0 ? (a + TT - 1) / TT : 0;
   g.S = n * g.nbt + g.nat;
+  g.SP = (nfact < 0) ? g.S : nfact * g.nbt;
   g.use_arrow = use_arrow && a > 0;
-  const bool base16 = ((uintptr_t)data % 16) == 0;
+  if (regions != nullptr) {
+    g.dg = const_cast<double*>(regions[0]);
+    g.lw = const_cast<double*>(regions[1]);
+    g.ar = const_cast<double*>(regions[2]);
+    g.tp = const_cast<double*>(regions[3]);
+    g.data = g.dg;
+  }
+  const bool base16 = al16(g.dg) && (n < 2 || al16(g.lw)) && (a == 0 || al16(g.ar));
   g.vec_b = base16 && (b % 2 == 0);
-  g.vec_a = g.vec_b && (a % 2 == 0);
+  g.vec_a = g.vec_b && (a % 2 == 0) && (a == 0 || al16(g.tp));
   return g;
 }
 
 // workspace: gstart | ctr, ticket, abort (one memset) | slots | W
 static size_t dag_ws(const Band& g, char* base, DagWs* o, size_t* zero_bytes) {
-  const int G = n_groups(g.S);
+  const int G = n_groups(g.SP);
   const size_t gs = align_up((size_t)(G + 1) * sizeof(int));
   const long long nctr = counter_elems(g.n, g.nbt, g.nat, g.S);
   const size_t cz = align_up((size_t)(nctr + 3) * sizeof(int));
@@ -515,17 +532,38 @@ long long stbta_storage_elems(int n, int b, int a) {
 
 size_t stbta_pobtaf_workspace_bytes(int n, int b, int a) {
   if (n < 1 || b < 1 || a < 0) return 0;
-  const Band g = make_band(nullptr, n, b, a, 1);
+  const Band g = make_band(nullptr, n, b, a, 1, -1);
   return dag_ws(g, nullptr, nullptr, nullptr);
 }
 
-
 int stbta_pobtaf(double* data, int n, int b, int a, int use_arrow, double* logdet_out, int* info,
                  void* workspace, size_t workspace_bytes, void* stream) {
-  if (data == nullptr || n < 1 || b < 1 || a < 0 || info == nullptr) return STBTA_EARG;
+  if (data == nullptr) return STBTA_EARG;
+  const long long bb = (long long)b * b;
+  double* diag = data;
+  double* lower = data + (long long)n * bb;
+  double* arrow = lower + (long long)(n - 1) * bb;
+  double* tip = arrow + (long long)n * a * b;
+  return stbta_pobtaf_ex(diag, lower, arrow, tip, n, b, a, use_arrow, -1, logdet_out, info,
+                         workspace, workspace_bytes, stream);
+}
+
+int stbta_pobtaf_ex(double* diag, double* lower, double* arrow, double* tip, int n, int b, int a,
+                    int use_arrow, int nfact, double* logdet_out, int* info, void* workspace,
+                    size_t workspace_bytes, void* stream) {
+  if (diag == nullptr || n < 1 || b < 1 || a < 0 || info == nullptr || nfact > n)
+    return STBTA_EARG;
+  if ((n > 1 && lower == nullptr) || (a > 0 && (arrow == nullptr || tip == nullptr)))
+    return STBTA_EARG;
   if (workspace_bytes < stbta_pobtaf_workspace_bytes(n, b, a)) return STBTA_EWORKSPACE;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  const Band g = make_band(data, n, b, a, use_arrow);
+  const double* regions[4] = {diag, lower, arrow, tip};
+  const Band g = make_band(regions, n, b, a, use_arrow, nfact);
+  if (g.SP == 0) {  // nothing to eliminate
+    int e = (int)cudaMemsetAsync(info, 0, sizeof(int), st);
+    if (!e && logdet_out) e = (int)cudaMemsetAsync(logdet_out, 0, sizeof(double), st);
+    return e;
+  }
   DagWs ws;
   size_t zbytes = 0;
   dag_ws(g, reinterpret_cast<char*>(workspace), &ws, &zbytes);
@@ -547,7 +585,7 @@ int stbta_pobtaf(double* data, int n, int b, int a, int use_arrow, double* logde
   count_launch();
   if ((e = (int)cudaGetLastError())) return e;
   if (logdet_out != nullptr) {
-    dag_logdet_kernel<<<1, 256, 0, st>>>(ws.slots, g.S, logdet_out);
+    dag_logdet_kernel<<<1, 256, 0, st>>>(ws.slots, g.SP, logdet_out);
     count_launch();
     if ((e = (int)cudaGetLastError())) return e;
   }

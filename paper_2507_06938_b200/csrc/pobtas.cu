@@ -190,8 +190,7 @@ __global__ void __launch_bounds__(PS_NT, 1) sweep_kernel(SweepArgs p) {
   for (int c = 0; c < NRC; ++c) acc[c] = 0.0;
 
   if (!FWD && g.use_arrow && h == 0 && r < extR) {  // x_R -= arrow[i][:, R]^T x_tip
-    const long long bb = (long long)g.b * g.b;
-    const double* arrow = g.data + (long long)(2 * g.n - 1) * bb + (long long)i * g.a * g.b;
+    const double* arrow = g.ar + (long long)i * g.a * g.b;
     const int col = (R % g.nbt) * 128 + r;
     for (int t = 0; t < g.a; ++t) {
       const double av = arrow[(long long)t * g.b + col];
@@ -310,8 +309,7 @@ __global__ void __launch_bounds__(PS_NT, 1) sweep_kernel(SweepArgs p) {
     if (c < nc) p.x[(row0 + rr) * p.ldx + c] = ybuf[e];
   }
   if (FWD && g.use_arrow) {  // arrow partials: part[R][t][c] = sum_r arrow[i][t][R0 + r] y[r][c]
-    const long long bb = (long long)g.b * g.b;
-    const double* arrow = g.data + (long long)(2 * g.n - 1) * bb + (long long)i * g.a * g.b;
+    const double* arrow = g.ar + (long long)i * g.a * g.b;
     const int col0 = (R % g.nbt) * 128;
     for (int t = warp; t < g.a; t += PS_NT / 32) {
       double s[NRC];
@@ -352,7 +350,7 @@ __global__ void tip_solve_kernel(SweepArgs p, int nparts, double* xtip, int mode
   const Band& g = p.g;
   const int a = g.a;
   const long long base = (long long)g.n * g.b;
-  const double* tip = g.data + (long long)(2 * g.n - 1) * g.b * g.b + (long long)g.n * a * g.b;
+  const double* tip = g.tp;
   double* v = p.x + base * p.ldx + c;
   const long long ld = p.ldx;
   if (mode == 0 && g.use_arrow) {
@@ -473,8 +471,22 @@ size_t stbta_pobtas_workspace_bytes(int n, int b, int a, int nrhs) {
 
 int stbta_pobtas(const double* factor, int n, int b, int a, int has_arrow, double* rhs, int nrhs,
                  int mode, void* workspace, size_t workspace_bytes, void* stream) {
-  if (factor == nullptr || rhs == nullptr || n < 1 || b < 1 || a < 0 || nrhs < 1 || mode < 0 ||
+  if (factor == nullptr) return STBTA_EARG;
+  const long long bb = (long long)b * b;
+  const double* lower = factor + (long long)n * bb;
+  const double* arrow = lower + (long long)(n - 1) * bb;
+  const double* tip = arrow + (long long)n * a * b;
+  return stbta_pobtas_ex(factor, lower, arrow, tip, n, b, a, has_arrow, rhs, nrhs, mode,
+                         workspace, workspace_bytes, stream);
+}
+
+int stbta_pobtas_ex(const double* diag, const double* lower, const double* arrow,
+                    const double* tip, int n, int b, int a, int has_arrow, double* rhs, int nrhs,
+                    int mode, void* workspace, size_t workspace_bytes, void* stream) {
+  if (diag == nullptr || rhs == nullptr || n < 1 || b < 1 || a < 0 || nrhs < 1 || mode < 0 ||
       mode > 2)
+    return STBTA_EARG;
+  if ((n > 1 && lower == nullptr) || (a > 0 && (arrow == nullptr || tip == nullptr)))
     return STBTA_EARG;
   if (workspace_bytes < stbta_pobtas_workspace_bytes(n, b, a, nrhs)) return STBTA_EWORKSPACE;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
@@ -482,11 +494,16 @@ int stbta_pobtas(const double* factor, int n, int b, int a, int has_arrow, doubl
   pobtas_ws(n, b, a, reinterpret_cast<char*>(workspace), &ws);
   SweepArgs p{};
   Band& g = p.g;
-  g.data = const_cast<double*>(factor);
   g.n = n; g.b = b; g.a = a;
+  g.dg = const_cast<double*>(diag);
+  g.lw = const_cast<double*>(lower);
+  g.ar = const_cast<double*>(arrow);
+  g.tp = const_cast<double*>(tip);
+  g.data = g.dg;
   g.nbt = (b + 127) / 128;
   g.nat = a > 0 ? (a + 127) / 128 : 0;
   g.S = n * g.nbt + g.nat;
+  g.SP = g.S;
   g.use_arrow = has_arrow && a > 0;
   g.vec_b = 0;
   g.vec_a = 0;

@@ -298,21 +298,32 @@ size_t stbta_pobtasi_workspace_bytes(int n, int b, int a) {
 
 int stbta_pobtasi(const double* factor, double* inv, int n, int b, int a, int has_arrow,
                   void* workspace, size_t workspace_bytes, void* stream) {
-  if (factor == nullptr || inv == nullptr || n < 1 || b < 1 || a < 0) return STBTA_EARG;
+  if (factor == nullptr || inv == nullptr) return STBTA_EARG;
+  const long long bb = (long long)b * b;
+  const double* L[4] = {factor, factor + n * bb, factor + (2LL * n - 1) * bb,
+                        factor + (2LL * n - 1) * bb + (long long)n * a * b};
+  double* X[4] = {inv, inv + n * bb, inv + (2LL * n - 1) * bb,
+                  inv + (2LL * n - 1) * bb + (long long)n * a * b};
+  return stbta_pobtasi_ex(L[0], L[1], L[2], L[3], X[0], X[1], X[2], X[3], n, b, a, has_arrow, -1,
+                          workspace, workspace_bytes, stream);
+}
+
+int stbta_pobtasi_ex(const double* Ld, const double* Ll, const double* La, const double* Lt,
+                     double* Xd, double* Xl, double* Xa, double* Xt, int n, int b, int a,
+                     int has_arrow, int nstart, void* workspace, size_t workspace_bytes,
+                     void* stream) {
+  if (Ld == nullptr || Xd == nullptr || n < 1 || b < 1 || a < 0 || nstart > n) return STBTA_EARG;
+  if ((n > 1 && (Ll == nullptr || Xl == nullptr)) ||
+      (a > 0 && (La == nullptr || Lt == nullptr || Xa == nullptr || Xt == nullptr)))
+    return STBTA_EARG;
   if (workspace_bytes < stbta_pobtasi_workspace_bytes(n, b, a)) return STBTA_EWORKSPACE;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   PobtasiWs ws;
   pobtasi_ws(n, b, a, reinterpret_cast<char*>(workspace), &ws);
   const long long bb = (long long)b * b;
-  const double* Ld = factor;
-  const double* Ll = Ld + n * bb;
-  const double* La = Ll + (n - 1) * bb;
-  const double* Lt = La + (long long)n * a * b;
-  double* Xd = inv;
-  double* Xl = Xd + n * bb;
-  double* Xa = Xl + (n - 1) * bb;
-  double* Xt = Xa + (long long)n * a * b;
   const bool arrow = has_arrow && a > 0;
+  const bool full = nstart < 0;  // otherwise X_tip, X_{nstart..} and X_a,{nstart..} are inputs
+  if (full) nstart = n;
   const size_t smem = SI_SMEM_DOUBLES * sizeof(double);
   static bool attr = false;
   int e;
@@ -322,16 +333,17 @@ int stbta_pobtasi(const double* factor, double* inv, int n, int b, int a, int ha
     if ((e = (int)cudaFuncSetAttribute(inv_offdiag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))) return e;
     attr = true;
   }
+  if (nstart == 0) return 0;
 
   // ---- 1. all inverses W_i (and W_tip) up front
   InvSet s{};
   s.L = Ld; s.W = ws.Wall; s.Lt = Lt; s.Wt = ws.Wt;
-  s.n = n; s.b = b; s.a = a; s.tmp = ws.tmp;
+  s.n = nstart; s.b = b; s.a = a; s.tmp = ws.tmp;
   s.ntb = (b + 127) / 128;
-  const int nta = a > 0 ? (a + 127) / 128 : 0;
-  const int nm = n + (a > 0 ? 1 : 0);
+  const int nta = (a > 0 && full) ? (a + 127) / 128 : 0;
+  const int nm = nstart + ((a > 0 && full) ? 1 : 0);
   const int ntm = s.ntb > nta ? s.ntb : nta;
-  if (a > 0 && (e = (int)cudaMemsetAsync(ws.Wt, 0, (size_t)a * a * sizeof(double), st))) return e;
+  if (a > 0 && full && (e = (int)cudaMemsetAsync(ws.Wt, 0, (size_t)a * a * sizeof(double), st))) return e;
   inv_diag_tiles_kernel<<<dim3(ntm, nm), SI_NT, smem, st>>>(s);
   count_launch();
   if ((e = (int)cudaGetLastError())) return e;
@@ -342,16 +354,17 @@ int stbta_pobtasi(const double* factor, double* inv, int n, int b, int a, int ha
   }
 
   // ---- 2. X_tip = W_t^T W_t ;  X_a = 0 when the arrow is inactive
-  if (a > 0) {
+  if (a > 0 && full) {
     TileJob j = job(Xt, a, a, a, 1.0);
     j.nprod = 1;
     j.p[0] = prod(ws.Wt, a, 1, ws.Wt, a, 1, a, 1.0);
     if ((e = launch_job(j, st))) return e;
-    if (!arrow && (e = (int)cudaMemsetAsync(Xa, 0, (size_t)n * a * b * sizeof(double), st))) return e;
   }
+  if (a > 0 && !arrow && (e = (int)cudaMemsetAsync(Xa, 0, (size_t)nstart * a * b * sizeof(double), st)))
+    return e;
 
-  // ---- 3. the recursion, i = n-1 .. 0
-  for (int i = n - 1; i >= 0; --i) {
+  // ---- 3. the recursion, i = nstart-1 .. 0
+  for (int i = nstart - 1; i >= 0; --i) {
     const double* W = ws.Wall + i * bb;
     const double* sub = (i < n - 1) ? Ll + i * bb : nullptr;
     const double* arr = arrow ? La + (long long)i * a * b : nullptr;
