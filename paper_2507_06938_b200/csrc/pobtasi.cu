@@ -56,69 +56,67 @@ struct TileJob {
   Prod p[2];
 };
 
-template <bool AKM, bool BKM>
-STBTA_DEV void run_prod(double (&acc)[SiCfg::MF][SiCfg::NF][2], const Prod& p, int tr, int tc,
+template <class Cfg, bool AKM, bool BKM>
+STBTA_DEV void run_prod(double (&acc)[Cfg::MF][Cfg::NF][2], const Prod& p, int tr, int tc,
                         int mrows, int ncols, double* smem) {
-  const Opnd A{AKM ? p.A + tr * 128 : p.A + (long long)tr * 128 * p.lda, p.lda,
-               p.arows_all ? 128 : mrows, 0};
-  const Opnd B{BKM ? p.B + tc * 128 : p.B + (long long)tc * 128 * p.ldb, p.ldb, ncols, 0};
-  Opnd a = A, b = B;
+  Opnd a{AKM ? p.A + tr * Cfg::BM : p.A + (long long)tr * Cfg::BM * p.lda, p.lda, mrows, 0};
+  Opnd b{BKM ? p.B + tc * 128 : p.B + (long long)tc * 128 * p.ldb, p.ldb, ncols, 0};
   a.vec = ((uintptr_t)a.p % 16 == 0) && (a.ld % 2 == 0);
   b.vec = ((uintptr_t)b.p % 16 == 0) && (b.ld % 2 == 0);
   const int kbeg = p.ktri ? tc * 128 : 0;
   if (kbeg >= p.K) return;
-  tile_mma<SiCfg, false, 0, AKM, BKM>(acc, a, b, p.K, 128, smem, kbeg);
+  tile_mma<Cfg, false, 0, AKM, BKM>(acc, a, b, p.K, 128, smem, kbeg);
 }
 
-STBTA_DEV void acc_neg(double (&acc)[SiCfg::MF][SiCfg::NF][2]) {
+template <class Cfg>
+STBTA_DEV void acc_neg(double (&acc)[Cfg::MF][Cfg::NF][2]) {
 #pragma unroll
-  for (int i = 0; i < SiCfg::MF; ++i)
+  for (int i = 0; i < Cfg::MF; ++i)
 #pragma unroll
-    for (int j = 0; j < SiCfg::NF; ++j) acc[i][j][0] = -acc[i][j][0], acc[i][j][1] = -acc[i][j][1];
+    for (int j = 0; j < Cfg::NF; ++j) acc[i][j][0] = -acc[i][j][0], acc[i][j][1] = -acc[i][j][1];
 }
 
+// One output tile (BM x 128) of a job: init, signed products, store (+ mirror).
+template <class Cfg>
 STBTA_DEV void tile_job_body(const TileJob& j, int tr, int tc, double* smem) {
-  const int mrows = min(128, j.M - tr * 128), ncols = min(128, j.N - tc * 128);
-  double acc[SiCfg::MF][SiCfg::NF][2];
+  const int mrows = min(Cfg::BM, j.M - tr * Cfg::BM), ncols = min(128, j.N - tc * 128);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, gq = lane >> 2, tq = lane & 3;
+  const int wm0 = (warp % Cfg::WARPS_M) * Cfg::WM, wn0 = (warp / Cfg::WARPS_M) * Cfg::WN;
+  const int r0 = tr * Cfg::BM, c0 = tc * 128;
+  double acc[Cfg::MF][Cfg::NF][2];
   if (j.init == 1) {
-    acc_load<SiCfg>(acc, j.C + (long long)tr * 128 * j.ldc + tc * 128, j.ldc, mrows, ncols, 0, 0);
-  } else if (j.init == 2) {
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, gq = lane >> 2, tq = lane & 3;
-    const int wm0 = (warp % SiCfg::WARPS_M) * SiCfg::WM, wn0 = (warp / SiCfg::WARPS_M) * SiCfg::WN;
+    acc_load<Cfg>(acc, j.C + (long long)r0 * j.ldc + c0, j.ldc, mrows, ncols, 0, 0);
+  } else if (j.init == 2) {  // acc[m][n] = ci[c0+n][r0+m]; ci lower triangular
 #pragma unroll
-    for (int i = 0; i < SiCfg::MF; ++i)
+    for (int i = 0; i < Cfg::MF; ++i)
 #pragma unroll
-      for (int jj = 0; jj < SiCfg::NF; ++jj)
+      for (int jj = 0; jj < Cfg::NF; ++jj)
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           const int m = wm0 + i * 8 + gq, n = wn0 + jj * 8 + 2 * tq + e;
-          // ci is lower triangular: element (tc*128+n, tr*128+m) vanishes above its diagonal
-          acc[i][jj][e] = (m < mrows && n < ncols && tc * 128 + n >= tr * 128 + m)
-                              ? __ldcg(j.ci + (long long)(tc * 128 + n) * j.ldci + tr * 128 + m)
+          acc[i][jj][e] = (m < mrows && n < ncols && c0 + n >= r0 + m)
+                              ? __ldcg(j.ci + (long long)(c0 + n) * j.ldci + r0 + m)
                               : 0.0;
         }
   } else {
-    acc_zero<SiCfg>(acc);
+    acc_zero<Cfg>(acc);
   }
   for (int q = 0; q < j.nprod; ++q) {
     const Prod& p = j.p[q];
-    if (p.sgn < 0) acc_neg(acc);
-    if (p.akm && p.bkm) run_prod<true, true>(acc, p, tr, tc, mrows, ncols, smem);
-    else if (p.akm) run_prod<true, false>(acc, p, tr, tc, mrows, ncols, smem);
-    else if (p.bkm) run_prod<false, true>(acc, p, tr, tc, mrows, ncols, smem);
-    else run_prod<false, false>(acc, p, tr, tc, mrows, ncols, smem);
-    if (p.sgn < 0) acc_neg(acc);
+    if (p.sgn < 0) acc_neg<Cfg>(acc);
+    if (p.akm && p.bkm) run_prod<Cfg, true, true>(acc, p, tr, tc, mrows, ncols, smem);
+    else if (p.akm) run_prod<Cfg, true, false>(acc, p, tr, tc, mrows, ncols, smem);
+    else if (p.bkm) run_prod<Cfg, false, true>(acc, p, tr, tc, mrows, ncols, smem);
+    else run_prod<Cfg, false, false>(acc, p, tr, tc, mrows, ncols, smem);
+    if (p.sgn < 0) acc_neg<Cfg>(acc);
   }
-  acc_store<SiCfg>(acc, j.C + (long long)tr * 128 * j.ldc + tc * 128, j.ldc, mrows, ncols, 0, 0, 0,
-                   j.alpha);
+  acc_store<Cfg>(acc, j.C + (long long)r0 * j.ldc + c0, j.ldc, mrows, ncols, 0, 0, 0, j.alpha);
   if (j.mirror && tr != tc) {  // transposed copy to tile (tc, tr)
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, gq = lane >> 2, tq = lane & 3;
-    const int wm0 = (warp % SiCfg::WARPS_M) * SiCfg::WM, wn0 = (warp / SiCfg::WARPS_M) * SiCfg::WN;
-    double* Ct = j.C + (long long)tc * 128 * j.ldc + tr * 128;
+    double* Ct = j.C + (long long)c0 * j.ldc + r0;
 #pragma unroll
-    for (int i = 0; i < SiCfg::MF; ++i)
+    for (int i = 0; i < Cfg::MF; ++i)
 #pragma unroll
-      for (int jj = 0; jj < SiCfg::NF; ++jj)
+      for (int jj = 0; jj < Cfg::NF; ++jj)
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           const int m = wm0 + i * 8 + gq, n = wn0 + jj * 8 + 2 * tq + e;
@@ -127,21 +125,34 @@ STBTA_DEV void tile_job_body(const TileJob& j, int tr, int tc, double* smem) {
   }
 }
 
-__global__ void __launch_bounds__(SI_NT, 1) tile_job_kernel(TileJob j, int tiles_n) {
+// Tile order: when a product's K range depends on the output column (W's
+// triangle), columns are issued heaviest first (tc = 0 has the full K), which
+// packs the second wave with the light tiles (longest-processing-time order).
+template <class Cfg>
+__global__ void __launch_bounds__(SI_NT, 1) tile_job_kernel(TileJob j, int tiles_m, int tiles_n,
+                                                           int colmajor) {
   extern __shared__ __align__(16) double smem[];
-  int t = blockIdx.x;
+  const int t = blockIdx.x;
   int tr, tc;
-  if (j.lower) {  // lower-triangular tile index
-    tr = (int)((sqrtf(8.0f * t + 1.0f) - 1.0f) * 0.5f);
-    if ((tr + 1) * (tr + 2) / 2 <= t) ++tr;
-    if (tr * (tr + 1) / 2 > t) --tr;
-    tc = t - tr * (tr + 1) / 2;
+  if (j.lower) {  // lower tiles, column by column: column c holds tiles_m - c tiles
+    int c = 0, rem = t;
+    while (rem >= tiles_m - c) {
+      rem -= tiles_m - c;
+      ++c;
+    }
+    tc = c;
+    tr = c + rem;
+  } else if (colmajor) {
+    tc = t / tiles_m;
+    tr = t % tiles_m;
   } else {
     tr = t / tiles_n;
     tc = t % tiles_n;
   }
-  tile_job_body(j, tr, tc, smem);
+  tile_job_body<Cfg>(j, tr, tc, smem);
 }
+
+using SiCfg32 = MmaCfg<32, 128, 32, 16, SI_NT, 16, 4>;
 
 // ------------------------------------------------------- inverses W_i, W_tip
 // Matrix z < nm: lower-triangular L at Lp(z) (ld, size), inverse written to
@@ -261,10 +272,20 @@ static size_t pobtasi_ws(int n, int b, int a, char* base, PobtasiWs* o) {
 }
 
 static int launch_job(const TileJob& j, cudaStream_t st) {
-  const int tm = (j.M + 127) / 128, tn = (j.N + 127) / 128;
+  const bool small = j.M <= 32 && !j.lower && !j.mirror;
+  const int bm = small ? 32 : 128;
+  const int tm = (j.M + bm - 1) / bm, tn = (j.N + 127) / 128;
   const int tiles = j.lower ? tm * (tm + 1) / 2 : tm * tn;
   if (tiles <= 0) return 0;
-  tile_job_kernel<<<tiles, SI_NT, SI_SMEM_DOUBLES * sizeof(double), st>>>(j, tn);
+  int colmajor = 0;
+  for (int q = 0; q < j.nprod; ++q) colmajor |= j.p[q].ktri;
+  if (small) {
+    tile_job_kernel<SiCfg32><<<tiles, SI_NT, SiCfg32::SMEM_DOUBLES * sizeof(double), st>>>(
+        j, tm, tn, colmajor);
+  } else {
+    tile_job_kernel<SiCfg><<<tiles, SI_NT, SiCfg::SMEM_DOUBLES * sizeof(double), st>>>(
+        j, tm, tn, colmajor);
+  }
   count_launch();
   return (int)cudaGetLastError();
 }
@@ -328,7 +349,8 @@ int stbta_pobtasi_ex(const double* Ld, const double* Ll, const double* La, const
   static bool attr = false;
   int e;
   if (!attr) {
-    if ((e = (int)cudaFuncSetAttribute(tile_job_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))) return e;
+    if ((e = (int)cudaFuncSetAttribute(tile_job_kernel<SiCfg>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(SiCfg::SMEM_DOUBLES * sizeof(double))))) return e;
+    if ((e = (int)cudaFuncSetAttribute(tile_job_kernel<SiCfg32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(SiCfg32::SMEM_DOUBLES * sizeof(double))))) return e;
     if ((e = (int)cudaFuncSetAttribute(inv_diag_tiles_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))) return e;
     if ((e = (int)cudaFuncSetAttribute(inv_offdiag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))) return e;
     attr = true;
