@@ -35,7 +35,7 @@
 namespace stbta {
 
 constexpr int DAG_NT = 256;
-using Cfg128 = MmaCfg<128, 128, 64, 32, DAG_NT>;
+using Cfg128 = MmaCfg<128, 128, 64, 32, DAG_NT, 32, 2>;
 using Cfg32 = MmaCfg<32, 128, 32, 16, DAG_NT>;
 constexpr int TRSM_SMEM_DOUBLES = 32 * 132 + 128 * 132 + 4 * 32 * PT_WLD;
 constexpr int cmax(int x, int y) { return x > y ? x : y; }

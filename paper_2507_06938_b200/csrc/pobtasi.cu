@@ -26,7 +26,7 @@
 namespace stbta {
 
 constexpr int SI_NT = 256;
-using SiCfg = MmaCfg<128, 128, 64, 32, SI_NT, 16, 4>;
+using SiCfg = MmaCfg<128, 128, 64, 32, SI_NT, 32, 2>;
 constexpr int SI_SMEM_DOUBLES =
     SiCfg::SMEM_DOUBLES > INV_SMEM_DOUBLES ? SiCfg::SMEM_DOUBLES : INV_SMEM_DOUBLES;
 
