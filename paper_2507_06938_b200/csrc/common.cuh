@@ -9,9 +9,30 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
+
 #define STBTA_DEV __device__ __forceinline__
 
 namespace stbta {
+
+// Kernel attributes (max dynamic shared memory) are per device: track, per
+// call site, the devices on which they have been set.
+inline int current_device_bit(unsigned long long* bit) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  *bit = 1ull << (dev & 63);
+  return dev;
+}
+inline bool attr_pending(const std::atomic<unsigned long long>& mask) {
+  unsigned long long bit;
+  current_device_bit(&bit);
+  return (mask.load(std::memory_order_relaxed) & bit) == 0;
+}
+inline void attr_mark(std::atomic<unsigned long long>& mask) {
+  unsigned long long bit;
+  current_device_bit(&bit);
+  mask.fetch_or(bit, std::memory_order_relaxed);
+}
 
 // Host-side count of kernel launches issued by the library (bench.py's
 // gpu_launches; read with stbta_launch_count()).

@@ -195,12 +195,12 @@ template <bool TA, bool TB, int BM, int BN, int WM, int WN, int BK, int STAGES>
 static int launch_cfg(const GemmArgs& g, cudaStream_t stream) {
   using Cfg = GemmCfg<TA, TB, BM, BN, WM, WN, BK, STAGES>;
   auto kern = dgemm_kernel<TA, TB, BM, BN, WM, WN, BK, STAGES>;
-  static bool attr_set = false;  // benign race: idempotent attribute write
-  if (!attr_set) {
+  static std::atomic<unsigned long long> attr_mask{0};  // per device
+  if (attr_pending(attr_mask)) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          Cfg::SMEM_BYTES);
     if (e != cudaSuccess) return (int)e;
-    attr_set = true;
+    attr_mark(attr_mask);
   }
   const int tiles_m = (g.M + BM - 1) / BM, tiles_n = (g.N + BN - 1) / BN;
   const bool two_a = g.A.r0 < (TA ? g.K : g.M);

@@ -568,12 +568,12 @@ int stbta_pobtaf_ex(double* diag, double* lower, double* arrow, double* tip, int
   size_t zbytes = 0;
   dag_ws(g, reinterpret_cast<char*>(workspace), &ws, &zbytes);
   ws.prof = debug_profile();
-  static bool attr_done = false;  // idempotent attribute write
-  if (!attr_done) {
+  static std::atomic<unsigned long long> attr_mask{0};  // per device
+  if (attr_pending(attr_mask)) {
     int e = (int)cudaFuncSetAttribute(pobtaf_dag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)DAG_SMEM_BYTES);
     if (e) return e;
-    attr_done = true;
+    attr_mark(attr_mask);
   }
   int e = (int)cudaMemsetAsync(info, 0, sizeof(int), st);
   if (e) return e;

@@ -409,8 +409,8 @@ static int run_sweeps(SweepArgs p, int mode, const PobtasWs& ws, cudaStream_t st
   const size_t fbytes = (size_t)(p.ntile + 1) * sizeof(int);  // flags + ticket
   const size_t smem = PS_SMEM_DOUBLES * sizeof(double);
   const size_t ismem = INV_SMEM_DOUBLES * sizeof(double);
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<unsigned long long> attr_mask{0};  // per device
+  if (attr_pending(attr_mask)) {
     int e1 = (int)cudaFuncSetAttribute(sweep_kernel<true, 1>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int e2 = (int)cudaFuncSetAttribute(sweep_kernel<false, 1>,
@@ -424,7 +424,7 @@ static int run_sweeps(SweepArgs p, int mode, const PobtasWs& ws, cudaStream_t st
     if (e1) return e1;
     if (e2) return e2;
     if (e3) return e3;
-    attr = true;
+    attr_mark(attr_mask);
   }
   int e;
   inv_tiles_kernel<<<p.ntile, PS_NT, ismem, st>>>(p.g, ws.winv);

@@ -346,14 +346,14 @@ int stbta_pobtasi_ex(const double* Ld, const double* Ll, const double* La, const
   const bool full = nstart < 0;  // otherwise X_tip, X_{nstart..} and X_a,{nstart..} are inputs
   if (full) nstart = n;
   const size_t smem = SI_SMEM_DOUBLES * sizeof(double);
-  static bool attr = false;
+  static std::atomic<unsigned long long> attr_mask{0};  // per device
   int e;
-  if (!attr) {
+  if (attr_pending(attr_mask)) {
     if ((e = (int)cudaFuncSetAttribute(tile_job_kernel<SiCfg>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(SiCfg::SMEM_DOUBLES * sizeof(double))))) return e;
     if ((e = (int)cudaFuncSetAttribute(tile_job_kernel<SiCfg32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(SiCfg32::SMEM_DOUBLES * sizeof(double))))) return e;
     if ((e = (int)cudaFuncSetAttribute(inv_diag_tiles_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))) return e;
     if ((e = (int)cudaFuncSetAttribute(inv_offdiag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))) return e;
-    attr = true;
+    attr_mark(attr_mask);
   }
   if (nstart == 0) return 0;
 
