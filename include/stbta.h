@@ -50,15 +50,17 @@ int stbta_pobtaf(double* data, int n, int b, int a, int use_arrow, double* logde
                  void* workspace, size_t workspace_bytes, void* stream);
 
 /* Region-pointer form of POBTAF (diag (n,b,b), lower (n-1,b,b), arrow (n,a,b),
- * tip (a,a) may live in separate buffers) with a partial-elimination count:
+ * tip (a,a) may live in separate buffers; the block rows may be padded to a
+ * row stride ldb >= b, e.g. b+1 for odd b so every row is 16-byte aligned)
+ * with a partial-elimination count:
  * nfact < 0 is the full factorization; 0 <= nfact <= n factorizes only the
  * first nfact time blocks, leaving the later blocks and the tip updated by
  * their Schur complement but unfactored, and
  * logdet_out covering the eliminated blocks only (time partitions of
  * bta_dist.d_factorize, reference bta_dist.py:174-254). */
 int stbta_pobtaf_ex(double* diag, double* lower, double* arrow, double* tip, int n, int b, int a,
-                    int use_arrow, int nfact, double* logdet_out, int* info, void* workspace,
-                    size_t workspace_bytes, void* stream);
+                    int ldb, int use_arrow, int nfact, double* logdet_out, int* info,
+                    void* workspace, size_t workspace_bytes, void* stream);
 
 /* ---------------------------------------------------------------- POBTAS --
  * Triangular solves against a POBTAF factor, in place on rhs (dim x nrhs,
@@ -69,10 +71,10 @@ size_t stbta_pobtas_workspace_bytes(int n, int b, int a, int nrhs);
 int stbta_pobtas(const double* factor, int n, int b, int a, int has_arrow, double* rhs, int nrhs,
                  int mode, void* workspace, size_t workspace_bytes, void* stream);
 
-/* Region-pointer form of POBTAS. */
+/* Region-pointer form of POBTAS (block row stride ldb >= b). */
 int stbta_pobtas_ex(const double* diag, const double* lower, const double* arrow,
-                    const double* tip, int n, int b, int a, int has_arrow, double* rhs, int nrhs,
-                    int mode, void* workspace, size_t workspace_bytes, void* stream);
+                    const double* tip, int n, int b, int a, int ldb, int has_arrow, double* rhs,
+                    int nrhs, int mode, void* workspace, size_t workspace_bytes, void* stream);
 
 /* --------------------------------------------------------------- POBTASI --
  * Selected inversion: the BTA-pattern entries of (L L^T)^-1 written to `inv`

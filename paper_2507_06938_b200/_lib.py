@@ -32,11 +32,13 @@ _SIGNATURES = {
     "stbta_pobtaf": (c_int, [c_vp, c_int, c_int, c_int, c_int, c_vp, c_vp, c_vp, c_size, c_vp]),
     "stbta_pobtaf_ex": (
         c_int,
-        [c_vp, c_vp, c_vp, c_vp, c_int, c_int, c_int, c_int, c_int, c_vp, c_vp, c_vp, c_size, c_vp],
+        [c_vp, c_vp, c_vp, c_vp, c_int, c_int, c_int, c_int, c_int, c_int, c_vp, c_vp, c_vp, c_size,
+         c_vp],
     ),
     "stbta_pobtas_ex": (
         c_int,
-        [c_vp, c_vp, c_vp, c_vp, c_int, c_int, c_int, c_int, c_vp, c_int, c_int, c_vp, c_size, c_vp],
+        [c_vp, c_vp, c_vp, c_vp, c_int, c_int, c_int, c_int, c_int, c_vp, c_int, c_int, c_vp, c_size,
+         c_vp],
     ),
     "stbta_pobtasi_ex": (
         c_int,

@@ -201,7 +201,7 @@ class _Chain:
                              dtype=torch.uint8, device=self.device)
             d, l, ar, tp = self.regions()
             _lib.check(
-                lib.stbta_pobtaf_ex(d, l, ar, tp, self.n_ext, self.b, self.ap,
+                lib.stbta_pobtaf_ex(d, l, ar, tp, self.n_ext, self.b, self.ap, self.b,
                                     int(self.chain_arrow), self.n_int, _lib.ptr(self.logdet_dev),
                                     _lib.ptr(self.info), _lib.ptr(ws), ws.numel(),
                                     _lib.stream_ptr()),
@@ -222,7 +222,7 @@ class _Chain:
                              device=self.device)
             _lib.check(
                 lib.stbta_pobtas_ex(_lib.ptr(self.diag), _lib.ptr(self.lower), None, None, n, b, 0,
-                                    0, _lib.ptr(rhs), k, 0, _lib.ptr(ws), ws.numel(),
+                                    b, 0, _lib.ptr(rhs), k, 0, _lib.ptr(ws), ws.numel(),
                                     _lib.stream_ptr()),
                 "stbta_pobtas_ex",
             )

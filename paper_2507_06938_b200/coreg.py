@@ -16,6 +16,8 @@ the per-evaluation work to the device:
 
 from dataclasses import dataclass
 
+import ctypes
+
 import numpy as np
 import scipy.sparse as sp
 import torch
@@ -281,6 +283,28 @@ def _same_discretization(spec):
     return True
 
 
+def padded_storage_elems(n, b, a, ldb):
+    """diag | lower | arrow with row stride ldb, then the a x a tip."""
+    return ((2 * n - 1) * b + n * a) * ldb + a * a
+
+
+def pad_offsets(off, n, b, a, ldb):
+    """Map flat reference-layout offsets (coreg.py:219-241 / BTAMatrix) to the
+    row-padded layout: every diag / lower / arrow row is one storage row of
+    length b; the tip is stored unchanged after them."""
+    if ldb == b:
+        return off
+    off = np.asarray(off, dtype=np.int64)
+    rows_total = (2 * n - 1) * b + n * a
+    split = rows_total * b
+    out = np.empty_like(off)
+    blk = off < split
+    r, c = np.divmod(off[blk], b)
+    out[blk] = r * ldb + c
+    out[~blk] = rows_total * ldb + (off[~blk] - split)
+    return out
+
+
 class AssemblyPlan:
     """theta -> (Q_p, Q_c) values in BTA storage, as one device kernel.
 
@@ -371,10 +395,16 @@ class AssemblyPlan:
             raise EnvelopeError("two structural nonzeros map to the same storage slot")
         self.n_entries = int(off.size)
         n, b, a = pmap.n_blocks, pmap.block_size, pmap.arrow_size
-        self.nstore = n * b * b + (n - 1) * b * b + n * a * b + a * a
+        self.nstore_flat = n * b * b + (n - 1) * b * b + n * a * b + a * a
+        # device workspaces pad odd block rows to an even stride, so every row
+        # of diag / lower / arrow is 16-byte aligned for the kernels' vector
+        # copies (C3: b = 5025); the padding column stays zero.
+        self.ldb = b + (b % 2)
+        self.nstore = padded_storage_elems(n, b, a, self.ldb)
+        poff = pad_offsets(off, n, b, a, self.ldb)
         tile = _lib.ASM_TILE
         ntiles = (self.nstore + tile - 1) // tile
-        starts = np.searchsorted(off, np.arange(ntiles + 1, dtype=np.int64) * tile)
+        starts = np.searchsorted(poff, np.arange(ntiles + 1, dtype=np.int64) * tile)
         # does any entry of the conditional pattern sit in an arrow block?
         base_ar = n * b * b + (n - 1) * b * b
         self.cond_has_arrow = bool(a > 0 and np.any((off >= base_ar) & (off < base_ar + n * a * b)))
@@ -383,7 +413,8 @@ class AssemblyPlan:
         self.h_pair = np.concatenate(pairs)[order]
         self.h_src = np.concatenate(srcs)[order]
         self.h_basis = table
-        self.d_offsets = torch.from_numpy(off).to(dev)
+        self.d_offsets = torch.from_numpy(off).to(dev)  # flat layout (quadform)
+        self.d_poffsets = torch.from_numpy(poff).to(dev) if self.ldb != b else self.d_offsets
         self.d_pair = torch.from_numpy(self.h_pair).to(dev)
         self.d_src = torch.from_numpy(self.h_src).to(dev)
         self.d_basis = torch.from_numpy(np.ascontiguousarray(table)).to(dev)
@@ -416,17 +447,36 @@ class AssemblyPlan:
         return cp, cc
 
     def assemble_host(self, coef):
-        """numpy evaluation of what :meth:`assemble` writes (host checks)."""
-        out = np.zeros(self.nstore)
+        """numpy evaluation of what :meth:`assemble` writes, in the flat
+        reference layout (host checks)."""
+        out = np.zeros(self.nstore_flat)
         vals = np.einsum("et,et->e", coef[self.h_pair], self.h_basis[self.h_src])
         out[self.h_offsets] = vals
         return out
+
+    def regions(self, data):
+        """(diag, lower, arrow, tip) device pointers of a padded workspace."""
+        n, b, a, ld = self.pmap.n_blocks, self.pmap.block_size, self.pmap.arrow_size, self.ldb
+        base = data.data_ptr()
+        lo = base + 8 * n * b * ld
+        ar = lo + 8 * (n - 1) * b * ld
+        tp = ar + 8 * n * a * ld
+        return [ctypes.c_void_p(p) for p in (base, lo, ar, tp)]
+
+    def unpad(self, data):
+        """Flat reference-layout copy of a padded workspace (tests / views)."""
+        n, b, a, ld = self.pmap.n_blocks, self.pmap.block_size, self.pmap.arrow_size, self.ldb
+        if ld == b:
+            return data
+        rows = (2 * n - 1) * b + n * a
+        blocks = data[: rows * ld].view(rows, ld)[:, :b].reshape(-1)
+        return torch.cat([blocks, data[rows * ld : rows * ld + a * a]])
 
     def assemble(self, data, coef_dev, stream=None):
         lib = _lib.load()
         _lib.check(
             lib.stbta_assemble(
-                _lib.ptr(data), self.nstore, _lib.ptr(self.d_starts), _lib.ptr(self.d_offsets),
+                _lib.ptr(data), self.nstore, _lib.ptr(self.d_starts), _lib.ptr(self.d_poffsets),
                 _lib.ptr(self.d_pair), _lib.ptr(self.d_src), _lib.ptr(self.d_basis),
                 _lib.ptr(coef_dev), self.n_terms, _lib.stream_ptr(stream),
             ),

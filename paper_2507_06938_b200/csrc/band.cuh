@@ -29,6 +29,7 @@ struct Band {
   double* data;  // flat BTA storage (unused when the region pointers are set)
   double *dg, *lw, *ar, *tp;  // diag (n,b,b) | lower (n-1,b,b) | arrow (n,a,b) | tip (a,a)
   int n, b, a;
+  int ldb;       // row stride of the diag / lower / arrow blocks (b, or b+1 padded)
   int nbt;       // tiles per time block
   int nat;       // arrow tiles
   int S;         // panels = n*nbt + nat
@@ -58,8 +59,8 @@ struct TilePtr {
 
 // storage of tile (R, C), R >= C in the band
 STBTA_DEV TilePtr tile_ptr(const Band& g, int R, int C) {
-  const long long b = g.b;
-  const long long bb = b * b;
+  const long long b = g.ldb;            // row stride
+  const long long bb = (long long)g.b * b;  // block stride
   double* diag = g.dg;
   double* lower = g.lw;
   double* arrow = g.ar;
@@ -76,7 +77,7 @@ STBTA_DEV TilePtr tile_ptr(const Band& g, int R, int C) {
   const int tc = C / g.nbt, jc = C % g.nbt;
   if (R >= NB) {
     const int qr = R - NB;
-    t.p = arrow + (long long)tc * g.a * b + (long long)qr * TT * b + jc * TT;
+    t.p = arrow + (long long)tc * g.a * b + (long long)qr * TT * b + jc * TT;  // arrow block: a x ldb
   } else {
     const int tr = R / g.nbt, jr = R % g.nbt;
     double* base = (tr == tc) ? diag + (long long)tc * bb : lower + (long long)tc * bb;
@@ -89,7 +90,7 @@ STBTA_DEV TilePtr tile_ptr(const Band& g, int R, int C) {
 
 // Upper-triangle mirror tile (C, R) of a same-block tile (R > C): diag storage.
 STBTA_DEV TilePtr tile_ptr_upper(const Band& g, int R, int C) {
-  const long long b = g.b;
+  const long long b = g.ldb;
   const int NB = g.n * g.nbt;
   if (C >= NB) {  // tip
     TilePtr p;
@@ -100,7 +101,7 @@ STBTA_DEV TilePtr tile_ptr_upper(const Band& g, int R, int C) {
   }
   const int t = C / g.nbt, jr = R % g.nbt, jc = C % g.nbt;
   TilePtr p;
-  p.p = g.dg + (long long)t * b * b + (long long)jc * TT * b + jr * TT;
+  p.p = g.dg + (long long)t * g.b * b + (long long)jc * TT * b + jr * TT;
   p.ld = b;
   p.vec = g.vec_b;
   return p;
@@ -163,6 +164,7 @@ inline long long counter_elems(int n, int nbt, int nat, int S) {
 
 // Region pointers of the reference's flat layout.
 inline void band_set_flat(Band& g, double* data) {
+  g.ldb = g.b;
   const long long bb = (long long)g.b * g.b;
   g.data = data;
   g.dg = data;

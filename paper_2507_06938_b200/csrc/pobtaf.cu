@@ -467,9 +467,10 @@ static bool al16(const void* p) { return ((uintptr_t)p % 16) == 0; }
 // factorize only the first nfact time blocks (partial elimination); the
 // remaining blocks and the tip receive their updates but stay unfactored.
 static Band make_band(const double* const* regions, int n, int b, int a, int use_arrow,
-                      int nfact) {
+                      int nfact, int ldb) {
   Band g{};
   g.n = n; g.b = b; g.a = a;
+  g.ldb = ldb;
   g.nbt = (b + TT - 1) / TT;
   g.nat = a > 0 ? (a + TT - 1) / TT : 0;
   g.S = n * g.nbt + g.nat;
@@ -483,7 +484,7 @@ static Band make_band(const double* const* regions, int n, int b, int a, int use
     g.data = g.dg;
   }
   const bool base16 = al16(g.dg) && (n < 2 || al16(g.lw)) && (a == 0 || al16(g.ar));
-  g.vec_b = base16 && (b % 2 == 0);
+  g.vec_b = base16 && (ldb % 2 == 0);
   g.vec_a = g.vec_b && (a % 2 == 0) && (a == 0 || al16(g.tp));
   return g;
 }
@@ -532,7 +533,7 @@ long long stbta_storage_elems(int n, int b, int a) {
 
 size_t stbta_pobtaf_workspace_bytes(int n, int b, int a) {
   if (n < 1 || b < 1 || a < 0) return 0;
-  const Band g = make_band(nullptr, n, b, a, 1, -1);
+  const Band g = make_band(nullptr, n, b, a, 1, -1, b);
   return dag_ws(g, nullptr, nullptr, nullptr);
 }
 
@@ -544,21 +545,21 @@ int stbta_pobtaf(double* data, int n, int b, int a, int use_arrow, double* logde
   double* lower = data + (long long)n * bb;
   double* arrow = lower + (long long)(n - 1) * bb;
   double* tip = arrow + (long long)n * a * b;
-  return stbta_pobtaf_ex(diag, lower, arrow, tip, n, b, a, use_arrow, -1, logdet_out, info,
+  return stbta_pobtaf_ex(diag, lower, arrow, tip, n, b, a, b, use_arrow, -1, logdet_out, info,
                          workspace, workspace_bytes, stream);
 }
 
 int stbta_pobtaf_ex(double* diag, double* lower, double* arrow, double* tip, int n, int b, int a,
-                    int use_arrow, int nfact, double* logdet_out, int* info, void* workspace,
-                    size_t workspace_bytes, void* stream) {
-  if (diag == nullptr || n < 1 || b < 1 || a < 0 || info == nullptr || nfact > n)
+                    int ldb, int use_arrow, int nfact, double* logdet_out, int* info,
+                    void* workspace, size_t workspace_bytes, void* stream) {
+  if (diag == nullptr || n < 1 || b < 1 || a < 0 || info == nullptr || nfact > n || ldb < b)
     return STBTA_EARG;
   if ((n > 1 && lower == nullptr) || (a > 0 && (arrow == nullptr || tip == nullptr)))
     return STBTA_EARG;
   if (workspace_bytes < stbta_pobtaf_workspace_bytes(n, b, a)) return STBTA_EWORKSPACE;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const double* regions[4] = {diag, lower, arrow, tip};
-  const Band g = make_band(regions, n, b, a, use_arrow, nfact);
+  const Band g = make_band(regions, n, b, a, use_arrow, nfact, ldb);
   if (g.SP == 0) {  // nothing to eliminate
     int e = (int)cudaMemsetAsync(info, 0, sizeof(int), st);
     if (!e && logdet_out) e = (int)cudaMemsetAsync(logdet_out, 0, sizeof(double), st);

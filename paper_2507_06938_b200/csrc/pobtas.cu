@@ -190,10 +190,10 @@ __global__ void __launch_bounds__(PS_NT, 1) sweep_kernel(SweepArgs p) {
   for (int c = 0; c < NRC; ++c) acc[c] = 0.0;
 
   if (!FWD && g.use_arrow && h == 0 && r < extR) {  // x_R -= arrow[i][:, R]^T x_tip
-    const double* arrow = g.ar + (long long)i * g.a * g.b;
+    const double* arrow = g.ar + (long long)i * g.a * g.ldb;
     const int col = (R % g.nbt) * 128 + r;
     for (int t = 0; t < g.a; ++t) {
-      const double av = arrow[(long long)t * g.b + col];
+      const double av = arrow[(long long)t * g.ldb + col];
 #pragma unroll
       for (int c = 0; c < NRC; ++c)
         if (c < nc) acc[c] -= av * p.xtip[t * NR + c];
@@ -309,14 +309,14 @@ __global__ void __launch_bounds__(PS_NT, 1) sweep_kernel(SweepArgs p) {
     if (c < nc) p.x[(row0 + rr) * p.ldx + c] = ybuf[e];
   }
   if (FWD && g.use_arrow) {  // arrow partials: part[R][t][c] = sum_r arrow[i][t][R0 + r] y[r][c]
-    const double* arrow = g.ar + (long long)i * g.a * g.b;
+    const double* arrow = g.ar + (long long)i * g.a * g.ldb;
     const int col0 = (R % g.nbt) * 128;
     for (int t = warp; t < g.a; t += PS_NT / 32) {
       double s[NRC];
 #pragma unroll
       for (int c = 0; c < NRC; ++c) s[c] = 0.0;
       for (int rr = lane; rr < extR; rr += 32) {
-        const double av = arrow[(long long)t * g.b + col0 + rr];
+        const double av = arrow[(long long)t * g.ldb + col0 + rr];
 #pragma unroll
         for (int c = 0; c < NRC; ++c) s[c] = fma(av, ybuf[rr * NR + c], s[c]);
       }
@@ -476,15 +476,15 @@ int stbta_pobtas(const double* factor, int n, int b, int a, int has_arrow, doubl
   const double* lower = factor + (long long)n * bb;
   const double* arrow = lower + (long long)(n - 1) * bb;
   const double* tip = arrow + (long long)n * a * b;
-  return stbta_pobtas_ex(factor, lower, arrow, tip, n, b, a, has_arrow, rhs, nrhs, mode,
+  return stbta_pobtas_ex(factor, lower, arrow, tip, n, b, a, b, has_arrow, rhs, nrhs, mode,
                          workspace, workspace_bytes, stream);
 }
 
 int stbta_pobtas_ex(const double* diag, const double* lower, const double* arrow,
-                    const double* tip, int n, int b, int a, int has_arrow, double* rhs, int nrhs,
-                    int mode, void* workspace, size_t workspace_bytes, void* stream) {
+                    const double* tip, int n, int b, int a, int ldb, int has_arrow, double* rhs,
+                    int nrhs, int mode, void* workspace, size_t workspace_bytes, void* stream) {
   if (diag == nullptr || rhs == nullptr || n < 1 || b < 1 || a < 0 || nrhs < 1 || mode < 0 ||
-      mode > 2)
+      mode > 2 || ldb < b)
     return STBTA_EARG;
   if ((n > 1 && lower == nullptr) || (a > 0 && (arrow == nullptr || tip == nullptr)))
     return STBTA_EARG;
@@ -495,6 +495,7 @@ int stbta_pobtas_ex(const double* diag, const double* lower, const double* arrow
   SweepArgs p{};
   Band& g = p.g;
   g.n = n; g.b = b; g.a = a;
+  g.ldb = ldb;
   g.dg = const_cast<double*>(diag);
   g.lw = const_cast<double*>(lower);
   g.ar = const_cast<double*>(arrow);

@@ -342,8 +342,7 @@ class ObjectiveEvaluator:
                     _lib.check(lib.stbta_rhs_combine(
                         _lib.ptr(s.rhs), _lib.ptr(self.d_U), _lib.ptr(tau_d), nv,
                         self.spec.joint_dim, _lib.stream_ptr(s.s_cond)), "rhs_combine")
-                    fac = bta.BTAFactor(self._view(s.ws_c), self.assembly.cond_has_arrow)
-                    bta._pobtas(fac, s.rhs, 0, stream=s.s_cond)
+                    self._pobtas(s.ws_c, self.assembly.cond_has_arrow, s.rhs, s.s_cond)
                     self.assembly.quadform(coef_p, s.rhs, s.partial, s.scal[2:3], s.s_cond)
                     _lib.check(lib.stbta_residual(
                         _lib.ptr(self.d_indptr), _lib.ptr(self.d_indices), _lib.ptr(self.d_vals),
@@ -390,19 +389,28 @@ class ObjectiveEvaluator:
                 mu = torch.zeros(self.spec.joint_dim, dtype=torch.float64, device=self.device)
         return value, mu
 
-    def _view(self, buf):
-        pm = self.pmap
-        return bta.BTAMatrix(pm.n_blocks, pm.block_size, pm.arrow_size, buf)
-
     def _pobtaf(self, buf, use_arrow, logdet_out, info_out, stream):
+        """POBTAF on a (row-padded) scratch workspace."""
         lib = _lib.load()
         pm = self.pmap
         n, b, a = pm.n_blocks, pm.block_size, pm.arrow_size
         nbytes = lib.stbta_pobtaf_workspace_bytes(n, b, a)
         ws = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
-        _lib.check(lib.stbta_pobtaf(
-            _lib.ptr(buf), n, b, a, int(bool(use_arrow) and a > 0), _lib.ptr(logdet_out),
-            _lib.ptr(info_out), _lib.ptr(ws), nbytes, _lib.stream_ptr(stream)), "stbta_pobtaf")
+        _lib.check(lib.stbta_pobtaf_ex(
+            *self.assembly.regions(buf), n, b, a, self.assembly.ldb,
+            int(bool(use_arrow) and a > 0), -1, _lib.ptr(logdet_out), _lib.ptr(info_out),
+            _lib.ptr(ws), nbytes, _lib.stream_ptr(stream)), "stbta_pobtaf_ex")
+
+    def _pobtas(self, buf, has_arrow, rhs, stream):
+        """In-place L L^T x = rhs against a (row-padded) scratch factor."""
+        lib = _lib.load()
+        pm = self.pmap
+        n, b, a = pm.n_blocks, pm.block_size, pm.arrow_size
+        nbytes = lib.stbta_pobtas_workspace_bytes(n, b, a, 1)
+        ws = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+        _lib.check(lib.stbta_pobtas_ex(
+            *self.assembly.regions(buf), n, b, a, self.assembly.ldb, int(bool(has_arrow)),
+            _lib.ptr(rhs), 1, 0, _lib.ptr(ws), nbytes, _lib.stream_ptr(stream)), "stbta_pobtas_ex")
 
     def evaluate(self, theta, counters=None):
         """(f_obj, conditional mean in variable-major order) (inla.py:320-371).
@@ -438,7 +446,10 @@ class ObjectiveEvaluator:
             ws = bta.BTAMatrix(self.pmap.n_blocks, self.pmap.block_size, self.pmap.arrow_size,
                                device=dev)
             coef = torch.from_numpy(np.ascontiguousarray(cc.ravel())).to(dev)
-            self.assembly.assemble(ws.data, coef)
+            padded = torch.empty(self.assembly.nstore, dtype=torch.float64, device=dev)
+            self.assembly.assemble(padded, coef)
+            ws.data.copy_(self.assembly.unpad(padded))
+            del padded
             factor = bta.factorize(ws, use_arrow=self.assembly.cond_has_arrow)
             if self.n_observations:
                 rhs = torch.empty(self.spec.joint_dim, dtype=torch.float64, device=dev)

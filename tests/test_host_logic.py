@@ -156,3 +156,27 @@ def test_objective_golden_spec_rebuild():
     g = golden("objective.npz")
     spec = spec_from_golden(g, "tri_")
     assert spec.n_processes == 3 and spec.joint_dim == 3 * (6 * 4 + 1)
+
+
+def test_padded_offsets_roundtrip():
+    """Row padding of odd block sizes: padded offsets address the same element."""
+    import torch
+
+    from paper_2507_06938_b200.coreg import pad_offsets, padded_storage_elems
+
+    rng = np.random.default_rng(3)
+    for n, b, a in [(3, 5, 2), (4, 7, 0), (2, 6, 3)]:
+        ld = b + (b % 2)
+        flat_n = n * b * b + (n - 1) * b * b + n * a * b + a * a
+        flat = rng.normal(size=flat_n)
+        off = np.sort(rng.choice(flat_n, size=flat_n // 2, replace=False)).astype(np.int64)
+        poff = pad_offsets(off, n, b, a, ld)
+        padded = np.zeros(padded_storage_elems(n, b, a, ld))
+        padded[poff] = flat[off]
+        rows = (2 * n - 1) * b + n * a
+        back = np.concatenate([padded[: rows * ld].reshape(rows, ld)[:, :b].ravel(),
+                               padded[rows * ld:]])
+        sel = np.zeros(flat_n, dtype=bool)
+        sel[off] = True
+        np.testing.assert_array_equal(back[sel], flat[sel])
+        assert np.all(np.diff(poff) > 0)
