@@ -57,6 +57,8 @@ def parse_args():
     p.add_argument("--cpu-sample-blocks", type=int, default=6)
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--no-inla", action="store_true",
+                   help="skip the C3 f_obj measurement (north-star model, rank 0 at N=1)")
     return p.parse_args()
 
 
@@ -174,6 +176,41 @@ def run_reference(args):
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+# --------------------------------------------------------------- C3 f_obj
+def measure_c3(dev):
+    """One trivariate (n_v=3, n_s=1675, n_t=48) f_obj at theta0 on this GPU --
+    the north-star model (BASELINE configs[2]); reported beside the C2 line with
+    the per-iteration estimate for a full 8-GPU box (1 line-search + 31
+    gradient evaluations, round-robin)."""
+    import numpy as np
+    import torch
+
+    from paper_2507_06938_b200 import inla
+    from paper_2507_06938_b200.synthetic import SyntheticSettings, generate_synthetic
+
+    th0 = np.array([-0.35, -0.25, -0.30, -0.20, -0.25, -0.25, 2.05, 2.05, 2.05, 0.05, 0.05,
+                    0.05, 0.65, -0.35, 0.35])
+    true = [-0.40, -0.30, -0.35, -0.25, -0.30, -0.30, 2.00, 2.00, 2.00, 0.00, 0.00, 0.00, 0.60,
+            -0.40, 0.30]
+    data = generate_synthetic(SyntheticSettings(3, 1675, 48, 1, 80400), true, seed=2, device=dev)
+    ev = inla.ObjectiveEvaluator(data.spec, prior=inla.ThetaPrior.for_dim(15, mean=th0, sd=2.0),
+                                 device=dev)
+    ev.objective(th0)
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(2):
+        t0 = time.perf_counter()
+        f = ev.objective(th0)
+        ts.append(time.perf_counter() - t0)
+    ev.release_workspaces()
+    t = min(ts)
+    return {"model": "C3 trivariate n_v=3 n_s=1675 n_t=48 n_r=1 (b=5025, N=241203), theta0",
+            "f_obj_s": t, "f_obj": f, "oracle_f_obj": -193110.15144130366,
+            "iteration_s_est_8gpu": t * (1 + -(-31 // 8)),
+            "iteration_s_est_1gpu": t * 32,
+            "cpu_reference_f_obj_s_survey": 67.7}
 
 
 # --------------------------------------------------------------- GPU leg
@@ -328,6 +365,10 @@ def main():
         cpu = {"value": flops_c / min(times_c) / 1e12, "unit": UNIT, "cores": cores, "kind": "port",
                "sample": sample, "seconds": min(times_c)}
 
+    inla_obj = None
+    if rank == 0 and world == 1 and not args.no_inla:
+        inla_obj = measure_c3(dev)
+
     if rank == 0:
         achieved = f_f / t_f / 1e12
         line = {
@@ -351,6 +392,7 @@ def main():
             "clocks": clk,
             "e2e": e2e,
             "cpu_baseline": cpu,
+            "inla": inla_obj,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
