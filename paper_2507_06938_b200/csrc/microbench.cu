@@ -53,6 +53,36 @@ static int mb_launch_bulk(const double* A, const double* B, double* C, int ntile
   return (int)cudaGetLastError();
 }
 
+template <class Cfg>
+__global__ void __launch_bounds__(Cfg::NT + 32, 1) mb_ws_kernel(const double* A, const double* B,
+                                                               double* C, int ntile, int reps,
+                                                               int K) {
+  extern __shared__ __align__(16) double smem[];
+  __shared__ __align__(8) unsigned long long bars[2 * Cfg::STAGES];
+  ws_bars_init<Cfg>(bars);
+  unsigned slab = 0;
+  const bool consumer = threadIdx.x < Cfg::NT;
+  for (int r = 0; r < reps; ++r) {
+    const int t = (blockIdx.x + r * gridDim.x) % ntile;
+    const double* a = A + (long long)t * 128 * K;
+    const double* b = B + (long long)t * 128 * K;
+    double* c = C + (long long)t * 128 * 128;
+    double acc[Cfg::MF][Cfg::NF][2];
+    if (consumer) acc_load<Cfg>(acc, c, 128, Cfg::BM, Cfg::BN, 0, 0);
+    tile_mma_ws<Cfg, true>(acc, a, K, b, K, K, smem, bars, slab);
+    if (consumer) acc_store<Cfg>(acc, c, 128, Cfg::BM, Cfg::BN, 0, 0, 0, 1.0);
+  }
+}
+
+template <class Cfg>
+static int mb_launch_ws(const double* A, const double* B, double* C, int ntile, int reps, int grid,
+                        cudaStream_t st, int K) {
+  const size_t smem = Cfg::SMEM_DOUBLES * sizeof(double);
+  cudaFuncSetAttribute(mb_ws_kernel<Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  mb_ws_kernel<Cfg><<<grid, Cfg::NT + 32, smem, st>>>(A, B, C, ntile, reps, K);
+  return (int)cudaGetLastError();
+}
+
 template <class Cfg, int DBG = 0>
 static int mb_launch(const double* A, const double* B, double* C, int ntile, int reps, int grid,
                      cudaStream_t st, int K) {
@@ -195,6 +225,9 @@ extern "C" int stbta_debug_tile_bench(int variant, const double* A, const double
     case 7: return mb_launch_bulk<MmaCfg<128, 128, 64, 32, 256, 32, 3>>(A, B, C, ntile, reps, grid, st, K);
     case 8: return mb_launch<MmaCfg<128, 128, 64, 32, 256, 32, 2>, 1>(A, B, C, ntile, reps, grid, st, K);
     case 9: return mb_launch<MmaCfg<128, 128, 64, 32, 256, 32, 2>, 2>(A, B, C, ntile, reps, grid, st, K);
+    case 10: return mb_launch_ws<MmaCfg<128, 128, 64, 32, 256, 16, 4>>(A, B, C, ntile, reps, grid, st, K);
+    case 11: return mb_launch_ws<MmaCfg<128, 128, 64, 32, 256, 32, 3>>(A, B, C, ntile, reps, grid, st, K);
+    case 12: return mb_launch_ws<MmaCfg<128, 128, 64, 32, 256, 16, 6>>(A, B, C, ntile, reps, grid, st, K);
     default: return -1;
   }
 }

@@ -9,7 +9,7 @@ for K in (128, 256, 1024):
     A = torch.randn(ntile, 128, K, dtype=torch.float64, device=dev)
     B = torch.randn(ntile, 128, K, dtype=torch.float64, device=dev)
     C = torch.zeros(ntile, 128, 128, dtype=torch.float64, device=dev)
-    for v in (3, 8, 9):
+    for v in (3, 10, 11, 12):
         grid, reps = 148, max(4, 5120 // K)
         rc = lib.stbta_debug_tile_bench(v, _lib.ptr(A), _lib.ptr(B), _lib.ptr(C), ntile, reps, grid, K, st)
         torch.cuda.synchronize()
