@@ -477,7 +477,10 @@ def eval_objective(theta, model):
 def _scalar_function(objective):
     if callable(objective) and not isinstance(objective, ObjectiveEvaluator):
         return objective
-    ev = objective if isinstance(objective, ObjectiveEvaluator) else ObjectiveEvaluator(objective)
+    if hasattr(objective, "objective"):  # an evaluator (or evaluator-like object)
+        ev = objective
+    else:  # a model spec
+        ev = ObjectiveEvaluator(objective)
     return lambda theta: -ev.objective(theta)
 
 
