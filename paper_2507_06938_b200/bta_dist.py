@@ -22,9 +22,10 @@ device kernels:
   recursion over the interior (``stbta_pobtasi_ex`` with ``nstart``), which is
   the reference's three-term interior recursion (bta_dist.py:508-602).
 
-Partitions may live on different GPUs (``devices``); a mapper runs them
-concurrently.  ``d_factorize_ranks`` is the one-process-per-GPU form used by
-``bench.py`` over NCCL.
+Partitions may live on different GPUs of one process (``devices``; a mapper
+runs them concurrently), or one per rank under torchrun:
+``d_factorize_nccl`` ships the chains and Schur pieces point-to-point over
+NCCL (NVLink) and factorizes the reduced system on the root.
 """
 
 import time
@@ -191,6 +192,14 @@ class _Chain:
     def regions(self):
         return [_lib.ptr(self.diag), _lib.ptr(self.lower), _lib.ptr(self.arrow), _lib.ptr(self.tip)]
 
+    def last_diag(self):
+        """Right separator block after the elimination (its reduced diagonal)."""
+        return self.diag[self.n_int]
+
+    def last_arrow(self):
+        """Arrowhead rows of the right separator block ([fill; f_right])."""
+        return self.arrow[self.n_int]
+
     def eliminate(self):
         """Partial POBTAF: factor the interior, leave the Schur pieces."""
         if self.n_int == 0:
@@ -317,6 +326,19 @@ def d_factorize(matrix, plan, counter=None, mapper=None, phase_times=None, devic
             _charge(counter, a**3, ch.n_int)
 
     seps = _separators(plan)
+    with _phase(phase_times, "reduced"):
+        reduced_factor = _reduce_and_factorize(matrix, plan, chains, use_arrow, counter)
+    return DistBTAFactor(plan, matrix, chains, reduced_factor, seps, use_arrow)
+
+
+def _reduce_and_factorize(matrix, plan, pieces, use_arrow, counter=None):
+    """Reduced 2(P-1)-block BTA over the separators from the original blocks
+    plus each partition's Schur pieces, summed in partition order
+    (bta_dist.py:322-350), factorized on the matrix's device.  ``pieces`` are
+    chains (or received copies) exposing n_int, off, left, right, tip, and the
+    last block's diag / arrow."""
+    b, a = matrix.block_size, matrix.arrow_size
+    seps = _separators(plan)
     dev = matrix.device
     n_red = len(seps)
     with torch.cuda.device(dev):
@@ -331,7 +353,7 @@ def d_factorize(matrix, plan, counter=None, mapper=None, phase_times=None, devic
         if a > 0:
             red.tip.copy_(matrix.tip)
         sp = {t: k for k, t in enumerate(seps)}
-        for ch in chains:  # partition order
+        for ch in pieces:  # partition order
             if ch.n_int == 0:
                 continue
             o = ch.off
@@ -342,19 +364,133 @@ def d_factorize(matrix, plan, counter=None, mapper=None, phase_times=None, devic
                     red.arrow[pos] += ch.tip[o:, :b].to(dev)
             if ch.right is not None:
                 pos = sp[ch.right]
-                red.diag[pos].copy_(_sym_lower(ch.diag[ch.n_int]).to(dev))
+                red.diag[pos].copy_(_sym_lower(ch.last_diag()).to(dev))
                 if use_arrow:
-                    red.arrow[pos].copy_(ch.arrow[ch.n_int, o:].to(dev))
+                    red.arrow[pos].copy_(ch.last_arrow()[o:].to(dev))
                 if ch.left is not None:
-                    red.lower[sp[ch.left]].copy_(ch.arrow[ch.n_int, :b].T.to(dev))
+                    red.lower[sp[ch.left]].copy_(ch.last_arrow()[:b].T.to(dev))
             if use_arrow:
                 red.tip += _sym_lower(ch.tip[o:, o:]).to(dev)
         try:
-            with _phase(phase_times, "reduced"):
-                reduced_factor = bta.factorize(red, counter=counter, use_arrow=use_arrow)
+            return bta.factorize(red, counter=counter, use_arrow=use_arrow)
         except FactorizationError as err:
             raise FactorizationError(seps[min(err.block_index, n_red - 1)], partition=-1) from None
-    return DistBTAFactor(plan, matrix, chains, reduced_factor, seps, use_arrow)
+
+
+class _Pieces:
+    """Schur pieces of a remote partition, received by the root."""
+
+    def __init__(self, ch, device):
+        self.index, self.left, self.right = ch.index, ch.left, ch.right
+        self.n_int, self.off, self.b = ch.n_int, ch.off, ch.b
+        f64 = dict(dtype=torch.float64, device=device)
+        self.tip = torch.empty_like(ch.tip, device=device)
+        self._diag = torch.empty(ch.b, ch.b, **f64) if ch.right is not None else None
+        self._arrow = torch.empty(ch.arrow.shape[1], ch.b, **f64) if ch.right is not None else None
+        self.logdet = 0.0
+
+    def last_diag(self):
+        return self._diag
+
+    def last_arrow(self):
+        return self._arrow
+
+
+def d_factorize_nccl(matrix, plan, group=None, root=0):
+    """PPOBTAF with one partition per rank (torchrun, NCCL over NVLink).
+
+    ``matrix`` (a BTAMatrix) is needed on ``root`` only; the other ranks pass
+    None.  The root ships each partition's extended chain to its rank
+    (point-to-point), every rank eliminates its interior concurrently, the
+    Schur pieces come back to the root, which assembles and factorizes the
+    reduced system in partition order.  Returns ``(logdet, chain)`` on every
+    rank (logdet broadcast from the root); a non-SPD pivot raises the same
+    FactorizationError on every rank.
+    """
+    import torch.distributed as dist
+
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    if plan.n_partitions != world:
+        raise PlanError(f"plan has {plan.n_partitions} partitions for {world} ranks")
+    dev = torch.device("cuda", torch.cuda.current_device())
+    if world == 1:  # sequential delegation on a copy (the input stays read-only)
+        f = bta.factorize(matrix.copy())
+        return bta.logdet(f), None
+    meta = torch.zeros(4, dtype=torch.int64, device=dev)
+    if rank == root:
+        meta[:] = torch.tensor([matrix.n_blocks, matrix.block_size, matrix.arrow_size,
+                                int(bta._arrow_nonzero(matrix))], device=dev)
+    dist.broadcast(meta, root, group=group)
+    n, b, a, use_arrow = (int(x) for x in meta.tolist())
+    if plan.n_blocks != n:
+        raise PlanError("plan does not match the matrix block count")
+    ranges = _partition_ranges(plan)
+    chains = {}
+    if rank == root:  # build and ship every chain, keep our own
+        for p, (lo, hi, left, right) in enumerate(ranges):
+            ch = _Chain(p, lo, hi, left, right, b, a, bool(use_arrow), dev)
+            ch.load(matrix)
+            if p == rank:
+                chains[p] = ch
+            else:
+                for t in (ch.diag, ch.lower, ch.arrow):
+                    dist.send(t, p, group=group)
+                del ch
+    else:
+        lo, hi, left, right = ranges[rank]
+        ch = _Chain(rank, lo, hi, left, right, b, a, bool(use_arrow), dev)
+        for t in (ch.diag, ch.lower, ch.arrow):
+            dist.recv(t, root, group=group)
+        chains[rank] = ch
+    mine = chains[rank]
+    err = torch.zeros(2, dtype=torch.int64, device=dev)
+    try:
+        mine.eliminate()
+    except FactorizationError as e:
+        err[:] = torch.tensor([1, e.block_index], device=dev)
+    errs = [torch.zeros_like(err) for _ in range(world)]
+    dist.all_gather(errs, err, group=group)
+    for p, e in enumerate(errs):
+        if int(e[0]):
+            raise FactorizationError(int(e[1]), partition=p)
+    # Schur pieces to the root
+    ld = torch.tensor([mine.logdet], dtype=torch.float64, device=dev)
+    if rank != root:
+        dist.send(ld, root, group=group)
+        dist.send(mine.tip, root, group=group)
+        if mine.right is not None:
+            dist.send(mine.last_diag().contiguous(), root, group=group)
+            dist.send(mine.last_arrow().contiguous(), root, group=group)
+        total = torch.zeros(1, dtype=torch.float64, device=dev)
+        dist.broadcast(total, root, group=group)
+        return float(total.item()), mine
+    pieces = []
+    interior = 0.0
+    for p, (lo, hi, left, right) in enumerate(ranges):
+        if p == rank:
+            pieces.append(mine)
+            interior += mine.logdet
+            continue
+        stub = _Chain.__new__(_Chain)
+        stub.index, stub.lo, stub.hi, stub.left, stub.right = p, lo, hi, left, right
+        stub.b, stub.n_int = b, hi - lo
+        stub.off = b if left is not None else 0
+        stub.tip = mine.tip.new_empty((max(stub.off + a, 1), max(stub.off + a, 1)))
+        stub.arrow = mine.arrow.new_empty((1, max(stub.off + a, 1), b))
+        pc = _Pieces(stub, dev)
+        buf = torch.zeros(1, dtype=torch.float64, device=dev)
+        dist.recv(buf, p, group=group)
+        pc.logdet = float(buf.item())
+        interior += pc.logdet
+        dist.recv(pc.tip, p, group=group)
+        if right is not None:
+            dist.recv(pc._diag, p, group=group)
+            dist.recv(pc._arrow, p, group=group)
+        pieces.append(pc)
+    reduced = _reduce_and_factorize(matrix, plan, pieces, bool(use_arrow))
+    total = torch.tensor([interior + bta.logdet(reduced)], dtype=torch.float64, device=dev)
+    dist.broadcast(total, root, group=group)
+    return float(total.item()), mine
 
 
 def d_logdet(factor):
