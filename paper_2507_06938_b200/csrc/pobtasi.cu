@@ -17,6 +17,8 @@
 //     either storage orientation so no transposes are materialised), with the
 //     triangular structure of W used to skip the zero K-range and X_ii formed
 //     on its lower tiles and mirrored.
+#include <cstdlib>
+
 #include "../../include/stbta.h"
 #include "band.cuh"
 #include "potrf_tile.cuh"
@@ -245,11 +247,245 @@ __global__ void __launch_bounds__(SI_NT, 1) inv_offdiag_kernel(InvSet s, int d) 
   acc_store<SiCfg>(acc, W + (long long)r * 128 * ld + c * 128, ld, er, ec, 0, 0, 0, -1.0);
 }
 
+// ------------------------------------------------- persistent recursion kernel
+// The whole recursion as one persistent kernel (one CTA per SM): output tiles
+// of all jobs are claimed from an atomic ticket in the recursion's order, and
+// each tile waits (acquire) only on the row / column stripes of earlier jobs
+// it reads, so there are no launch gaps and no half-empty last waves:
+//   per block i, tickets  Ta_i | T1_i | Xa_i | Xl_i | T3_i | Xii_i
+//   Ta_i  = X_tip L_a,i + X_a,i+1 L_i+1,i        waits X_a,i+1 (all), X_tip (all)
+//   T1_i  = X_i+1,i+1 L_i+1,i + X_a,i+1^T L_a,i  waits row+col tr of Xii_i+1, col tr of X_a,i+1
+//   X_a,i = -Ta_i W_i                            waits Ta_i (all)
+//   X_l,i = -T1_i W_i                            waits row tr of T1_i
+//   T3_i  = W_i^T - X_l,i^T L_i+1,i - X_a,i^T L_a,i   waits col tr of X_l,i and X_a,i
+//   Xii_i = T3_i W_i (lower, mirrored)           waits row tr of T3_i
+// Every wait targets a strictly earlier ticket, so the schedule cannot
+// deadlock.  T1/T3/Ta alternate between two buffers by block parity; the
+// transitive waits above guarantee a buffer's readers have finished before
+// it is rewritten two blocks later.  Rows are issued last-first so the
+// (row, column) crosses of Xii that T1 of the next block needs complete early.
+enum { K_TA = 0, K_T1 = 1, K_XA = 2, K_XL = 3, K_T3 = 4, K_XII = 5, K_NKIND = 6 };
+
+struct SiParams {
+  const double *Ld, *Ll, *La, *Lt;
+  double *Xd, *Xl, *Xa, *Xt;
+  const double *W, *Wt;
+  double *T1[2], *T3[2], *Ta[2];
+  int n, b, a, arrow, nstart, tip;
+  int ntb;       // 128-tiles per block dimension
+  int tma;       // row tiles of the a-row jobs (1 when a <= 32: 32-row tiles)
+  int tnt;       // column tiles of the tip job
+  int cs, cm;    // counter slot stride, column offset inside a slot
+  int p0;        // tickets of the tip job
+  int c_last;    // tickets of block n-1 (no sub-diagonal)
+  int c_full;    // tickets of every other block
+  long long total;
+  int* ctr;
+  unsigned long long* ticket;
+  int* abortw;  // stays zero (no failure mode in the recursion)
+};
+
+struct Shape {
+  int tm, tn, lower, small;
+};
+
+__host__ __device__ inline Shape kind_shape(const SiParams& P, int kind, int has_sub) {
+  switch (kind) {
+    case K_TA:
+    case K_XA: return {P.arrow ? P.tma : 0, P.ntb, 0, P.a <= 32};
+    case K_T1:
+    case K_XL: return {has_sub ? P.ntb : 0, P.ntb, 0, 0};
+    case K_T3: return {P.ntb, P.ntb, 0, 0};
+    default: return {P.ntb, P.ntb, 1, 0};
+  }
+}
+__host__ __device__ inline int shape_tiles(const Shape& s) {
+  return s.lower ? s.tm * (s.tm + 1) / 2 : s.tm * s.tn;
+}
+
+STBTA_DEV int* ctr_slot(const SiParams& P, int i, int kind) {  // i < 0: tip job
+  if (i < 0) return P.ctr;
+  return P.ctr + (long long)(1 + (long long)(P.nstart - 1 - i) * K_NKIND + kind) * P.cs;
+}
+
+// Builds the job (kind, i) exactly as the per-launch recursion would.
+STBTA_DEV void make_job(const SiParams& P, int kind, int i, TileJob& j) {
+  const long long bb = (long long)P.b * P.b;
+  const int b = P.b, a = P.a;
+  const double* W = P.W + i * bb;
+  const double* sub = (i < P.n - 1) ? P.Ll + i * bb : nullptr;
+  const double* arr = P.arrow ? P.La + (long long)i * a * b : nullptr;
+  const int par = i & 1;
+  j = TileJob{};
+  j.alpha = 1.0;
+  auto pr = [](const double* A, long long lda, int akm, const double* B, long long ldb, int bkm,
+               int K, double sgn, int ktri) {
+    Prod p{};
+    p.A = A; p.lda = lda; p.akm = akm; p.B = B; p.ldb = ldb; p.bkm = bkm;
+    p.K = K; p.sgn = sgn; p.ktri = ktri;
+    return p;
+  };
+  switch (kind) {
+    case K_TA:
+      j.C = P.Ta[par]; j.ldc = b; j.M = a; j.N = b;
+      j.p[j.nprod++] = pr(P.Xt, a, 0, arr, b, 1, a, 1.0, 0);
+      if (sub) j.p[j.nprod++] = pr(P.Xa + (long long)(i + 1) * a * b, b, 0, sub, b, 1, b, 1.0, 0);
+      break;
+    case K_T1:
+      j.C = P.T1[par]; j.ldc = b; j.M = b; j.N = b;
+      j.p[j.nprod++] = pr(P.Xd + (i + 1) * bb, b, 0, sub, b, 1, b, 1.0, 0);
+      if (arr) j.p[j.nprod++] = pr(P.Xa + (long long)(i + 1) * a * b, b, 1, arr, b, 1, a, 1.0, 0);
+      break;
+    case K_XA:
+      j.C = P.Xa + (long long)i * a * b; j.ldc = b; j.M = a; j.N = b; j.alpha = -1.0;
+      j.p[j.nprod++] = pr(P.Ta[par], b, 0, W, b, 1, b, 1.0, 1);
+      break;
+    case K_XL:
+      j.C = P.Xl + i * bb; j.ldc = b; j.M = b; j.N = b; j.alpha = -1.0;
+      j.p[j.nprod++] = pr(P.T1[par], b, 0, W, b, 1, b, 1.0, 1);
+      break;
+    case K_T3:
+      j.C = P.T3[par]; j.ldc = b; j.M = b; j.N = b;
+      j.init = 2; j.ci = W; j.ldci = b;
+      if (sub) j.p[j.nprod++] = pr(P.Xl + i * bb, b, 1, sub, b, 1, b, -1.0, 0);
+      if (arr) j.p[j.nprod++] = pr(P.Xa + (long long)i * a * b, b, 1, arr, b, 1, a, -1.0, 0);
+      break;
+    default:  // K_XII
+      j.C = P.Xd + i * bb; j.ldc = b; j.M = b; j.N = b;
+      j.lower = 1; j.mirror = 1;
+      j.p[j.nprod++] = pr(P.T3[par], b, 0, W, b, 1, b, 1.0, 1);
+      break;
+  }
+}
+
+// (tr, tc) of the t-th tile of a job: rows last-first, columns first-first
+// (the heaviest K of a W-triangular product first within a row).
+STBTA_DEV void tile_of(const Shape& s, int t, int& tr, int& tc) {
+  if (s.lower) {
+    int r = s.tm - 1;
+    while (t > r) {
+      t -= r + 1;
+      --r;
+    }
+    tr = r;
+    tc = t;
+  } else {
+    tr = s.tm - 1 - t / s.tn;
+    tc = t % s.tn;
+  }
+}
+
+STBTA_DEV void wait_all(const SiParams& P, int kind, int i, int tr) {
+  // thread 0 only
+  const bool sub = i < P.n - 1;
+  const bool prev = i + 1 < P.nstart;  // block i+1 computed in this call
+  switch (kind) {
+    case K_TA:
+      if (P.tip) spin_geq(ctr_slot(P, -1, 0) + 2 * P.cm, P.p0, P.abortw);
+      if (sub && prev)
+        spin_geq(ctr_slot(P, i + 1, K_XA) + 2 * P.cm, P.tma * P.ntb, P.abortw);
+      break;
+    case K_T1:
+      if (prev) {
+        const int* x = ctr_slot(P, i + 1, K_XII);
+        spin_geq(x + tr, tr + 1, P.abortw);
+        spin_geq(x + P.cm + tr, P.ntb - tr, P.abortw);
+        if (P.arrow) spin_geq(ctr_slot(P, i + 1, K_XA) + P.cm + tr, P.tma, P.abortw);
+      }
+      break;
+    case K_XA: spin_geq(ctr_slot(P, i, K_TA) + 2 * P.cm, P.tma * P.ntb, P.abortw); break;
+    case K_XL: spin_geq(ctr_slot(P, i, K_T1) + tr, P.ntb, P.abortw); break;
+    case K_T3:
+      if (sub) spin_geq(ctr_slot(P, i, K_XL) + P.cm + tr, P.ntb, P.abortw);
+      if (P.arrow) {
+        spin_geq(ctr_slot(P, i, K_XA) + P.cm + tr, P.tma, P.abortw);
+      }
+      break;
+    default: spin_geq(ctr_slot(P, i, K_T3) + tr, P.ntb, P.abortw); break;
+  }
+}
+
+__global__ void __launch_bounds__(SI_NT, 1) sinv_persistent_kernel(SiParams P) {
+  extern __shared__ __align__(16) double smem[];
+  __shared__ TileJob s_job;
+  __shared__ int s_info[4];  // kind, i, tr, tc (+ small flag in kind's high bit)
+  for (;;) {
+    if (threadIdx.x == 0) {
+      long long t = (long long)atomicAdd(P.ticket, 1ull);
+      int kind = -1, i = -1, tr = 0, tc = 0;
+      Shape sh{0, 0, 0, 0};
+      if (t < P.p0) {  // X_tip = W_t^T W_t
+        kind = 0;
+        sh = {P.tma, P.tnt, 0, P.a <= 32};
+        tile_of(sh, (int)t, tr, tc);
+        TileJob j{};
+        j.C = P.Xt; j.ldc = P.a; j.M = P.a; j.N = P.a; j.alpha = 1.0; j.nprod = 1;
+        j.p[0].A = P.Wt; j.p[0].lda = P.a; j.p[0].akm = 1;
+        j.p[0].B = P.Wt; j.p[0].ldb = P.a; j.p[0].bkm = 1;
+        j.p[0].K = P.a; j.p[0].sgn = 1.0;
+        s_job = j;
+      } else if (t < P.total) {
+        t -= P.p0;
+        int step;
+        if (P.nstart == P.n) {
+          if (t < P.c_last) step = 0;
+          else { t -= P.c_last; step = 1 + (int)(t / P.c_full); t %= P.c_full; }
+        } else {
+          step = (int)(t / P.c_full);
+          t %= P.c_full;
+        }
+        i = P.nstart - 1 - step;
+        const int has_sub = i < P.n - 1;
+        for (kind = 0; kind < K_NKIND; ++kind) {
+          sh = kind_shape(P, kind, has_sub);
+          const int nt = shape_tiles(sh);
+          if (t < nt) break;
+          t -= nt;
+        }
+        tile_of(sh, (int)t, tr, tc);
+        wait_all(P, kind, i, tr);
+        TileJob j;
+        make_job(P, kind, i, j);
+        s_job = j;
+      } else {
+        kind = -2;
+      }
+      s_info[0] = kind | (sh.small ? 0x100 : 0);
+      s_info[1] = i;
+      s_info[2] = tr;
+      s_info[3] = tc;
+    }
+    __syncthreads();
+    const int kinfo = s_info[0], i = s_info[1], tr = s_info[2], tc = s_info[3];
+    if (kinfo == -2) return;
+    if (kinfo & 0x100) tile_job_body<SiCfg32>(s_job, tr, tc, smem);
+    else tile_job_body<SiCfg>(s_job, tr, tc, smem);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int* c = ctr_slot(P, i, kinfo & 0xff);
+      __threadfence();
+      atomicAdd(c + tr, 1);
+      atomicAdd(c + P.cm + tc, 1);
+      atomicAdd(c + 2 * P.cm, 1);
+    }
+  }
+}
+
 static size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 
 struct PobtasiWs {
-  double *Wall, *Wt, *T1, *T3, *Ta, *tmp;
+  double *Wall, *Wt, *T1[2], *T3[2], *Ta[2], *tmp;
+  int* ctr;  // ticket (8 bytes) | abort word | pad | tile counters
+  size_t ctr_bytes;
 };
+
+static int si_cm(int b, int a) {
+  const int ntb = (b + 127) / 128;
+  const int tma = a <= 32 ? 1 : (a + 127) / 128;
+  const int tnt = (a + 127) / 128;
+  int cm = ntb > tma ? ntb : tma;
+  return cm > tnt ? cm : tnt;
+}
 
 static size_t pobtasi_ws(int n, int b, int a, char* base, PobtasiWs* o) {
   const int ntb = (b + 127) / 128;
@@ -260,15 +496,25 @@ static size_t pobtasi_ws(int n, int b, int a, char* base, PobtasiWs* o) {
   const size_t bb = align_up((size_t)b * b * sizeof(double));
   const size_t ta = align_up((size_t)(a > 0 ? a : 1) * b * sizeof(double));
   const size_t tmp = align_up((size_t)(n + 1) * ntm * 128 * 128 * sizeof(double));
+  const size_t ctr = align_up(16 + (size_t)(1 + 6LL * n) * (2 * si_cm(b, a) + 1) * sizeof(int));
   if (o) {
-    o->Wall = reinterpret_cast<double*>(base);
-    o->Wt = reinterpret_cast<double*>(base + wall);
-    o->T1 = reinterpret_cast<double*>(base + wall + wt);
-    o->T3 = reinterpret_cast<double*>(base + wall + wt + bb);
-    o->Ta = reinterpret_cast<double*>(base + wall + wt + 2 * bb);
-    o->tmp = reinterpret_cast<double*>(base + wall + wt + 2 * bb + ta);
+    char* p = base;
+    o->Wall = reinterpret_cast<double*>(p); p += wall;
+    o->Wt = reinterpret_cast<double*>(p); p += wt;
+    for (int q = 0; q < 2; ++q) { o->T1[q] = reinterpret_cast<double*>(p); p += bb; }
+    for (int q = 0; q < 2; ++q) { o->T3[q] = reinterpret_cast<double*>(p); p += bb; }
+    for (int q = 0; q < 2; ++q) { o->Ta[q] = reinterpret_cast<double*>(p); p += ta; }
+    o->tmp = reinterpret_cast<double*>(p); p += tmp;
+    o->ctr = reinterpret_cast<int*>(p);
+    o->ctr_bytes = ctr;
   }
-  return wall + wt + 2 * bb + ta + tmp;
+  return wall + wt + 4 * bb + 2 * ta + tmp + ctr;
+}
+
+static int sm_count() {
+  int dev = 0, v = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+  return v;
 }
 
 static int launch_job(const TileJob& j, cudaStream_t st) {
@@ -375,15 +621,62 @@ int stbta_pobtasi_ex(const double* Ld, const double* Ll, const double* La, const
     if ((e = (int)cudaGetLastError())) return e;
   }
 
-  // ---- 2. X_tip = W_t^T W_t ;  X_a = 0 when the arrow is inactive
+  if (a > 0 && !arrow && (e = (int)cudaMemsetAsync(Xa, 0, (size_t)nstart * a * b * sizeof(double), st)))
+    return e;
+
+  static const bool use_launches = [] {
+    const char* v = getenv("STBTA_SINV_LAUNCHES");
+    return v && v[0] == '1';
+  }();
+  if (!use_launches) {
+    // ---- 2+3. X_tip and the whole recursion in one persistent kernel
+    SiParams P{};
+    P.Ld = Ld; P.Ll = Ll; P.La = La; P.Lt = Lt;
+    P.Xd = Xd; P.Xl = Xl; P.Xa = Xa; P.Xt = Xt;
+    P.W = ws.Wall; P.Wt = ws.Wt;
+    for (int q = 0; q < 2; ++q) { P.T1[q] = ws.T1[q]; P.T3[q] = ws.T3[q]; P.Ta[q] = ws.Ta[q]; }
+    P.n = n; P.b = b; P.a = a; P.arrow = arrow; P.nstart = nstart; P.tip = a > 0 && full;
+    P.ntb = (b + 127) / 128;
+    P.tma = a <= 32 ? 1 : (a + 127) / 128;
+    P.tnt = (a + 127) / 128;
+    P.cm = si_cm(b, a);
+    P.cs = 2 * P.cm + 1;
+    P.p0 = P.tip ? P.tma * P.tnt : 0;
+    P.c_last = P.c_full = 0;
+    for (int k = 0; k < K_NKIND; ++k) {
+      P.c_last += shape_tiles(kind_shape(P, k, 0));
+      P.c_full += shape_tiles(kind_shape(P, k, 1));
+    }
+    P.total = P.p0 + (nstart == n ? P.c_last + (long long)(nstart - 1) * P.c_full
+                                   : (long long)nstart * P.c_full);
+    P.ticket = reinterpret_cast<unsigned long long*>(ws.ctr);
+    P.abortw = ws.ctr + 2;
+    P.ctr = ws.ctr + 4;
+    if ((e = (int)cudaMemsetAsync(ws.ctr, 0, ws.ctr_bytes, st))) return e;
+    static std::atomic<unsigned long long> pmask{0};
+    if (attr_pending(pmask)) {
+      if ((e = (int)cudaFuncSetAttribute(sinv_persistent_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(SiCfg::SMEM_DOUBLES * sizeof(double))))) return e;
+      attr_mark(pmask);
+    }
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sinv_persistent_kernel, SI_NT,
+                                                  SiCfg::SMEM_DOUBLES * sizeof(double));
+    if (occ < 1) return STBTA_EARG;
+    long long grid = (long long)sm_count() * occ;
+    if (grid > P.total) grid = P.total;
+    if (grid < 1) return 0;
+    sinv_persistent_kernel<<<(int)grid, SI_NT, SiCfg::SMEM_DOUBLES * sizeof(double), st>>>(P);
+    count_launch();
+    return (int)cudaGetLastError();
+  }
+
+  // ---- per-launch variant (STBTA_SINV_LAUNCHES=1; A/B reference for the persistent kernel)
   if (a > 0 && full) {
     TileJob j = job(Xt, a, a, a, 1.0);
     j.nprod = 1;
     j.p[0] = prod(ws.Wt, a, 1, ws.Wt, a, 1, a, 1.0);
     if ((e = launch_job(j, st))) return e;
   }
-  if (a > 0 && !arrow && (e = (int)cudaMemsetAsync(Xa, 0, (size_t)nstart * a * b * sizeof(double), st)))
-    return e;
 
   // ---- 3. the recursion, i = nstart-1 .. 0
   for (int i = nstart - 1; i >= 0; --i) {
@@ -392,28 +685,28 @@ int stbta_pobtasi_ex(const double* Ld, const double* Ll, const double* La, const
     const double* arr = arrow ? La + (long long)i * a * b : nullptr;
     if (sub) {
       // T1 = X_{i+1,i+1} L_{i+1,i} (+ X_{a,i+1}^T L_{a,i})
-      TileJob j = job(ws.T1, b, b, b, 1.0);
+      TileJob j = job(ws.T1[0], b, b, b, 1.0);
       j.p[j.nprod++] = prod(Xd + (i + 1) * bb, b, 0, sub, b, 1, b, 1.0);
       if (arr) j.p[j.nprod++] = prod(Xa + (long long)(i + 1) * a * b, b, 1, arr, b, 1, a, 1.0);
       if ((e = launch_job(j, st))) return e;
       // X_{i+1,i} = -T1 W
       TileJob j2 = job(Xl + i * bb, b, b, b, -1.0);
-      j2.p[j2.nprod++] = prod(ws.T1, b, 0, W, b, 1, b, 1.0, 1);
+      j2.p[j2.nprod++] = prod(ws.T1[0], b, 0, W, b, 1, b, 1.0, 1);
       if ((e = launch_job(j2, st))) return e;
     }
     if (arr) {
       // Ta = X_tip L_{a,i} (+ X_{a,i+1} L_{i+1,i});  X_{a,i} = -Ta W
-      TileJob j = job(ws.Ta, b, a, b, 1.0);
+      TileJob j = job(ws.Ta[0], b, a, b, 1.0);
       j.p[j.nprod++] = prod(Xt, a, 0, arr, b, 1, a, 1.0);
       if (sub) j.p[j.nprod++] = prod(Xa + (long long)(i + 1) * a * b, b, 0, sub, b, 1, b, 1.0);
       if ((e = launch_job(j, st))) return e;
       TileJob j2 = job(Xa + (long long)i * a * b, b, a, b, -1.0);
-      j2.p[j2.nprod++] = prod(ws.Ta, b, 0, W, b, 1, b, 1.0, 1);
+      j2.p[j2.nprod++] = prod(ws.Ta[0], b, 0, W, b, 1, b, 1.0, 1);
       if ((e = launch_job(j2, st))) return e;
     }
     // T3 = W^T - X_{i+1,i}^T L_{i+1,i} - X_{a,i}^T L_{a,i}
     {
-      TileJob j = job(ws.T3, b, b, b, 1.0);
+      TileJob j = job(ws.T3[0], b, b, b, 1.0);
       j.init = 2;
       j.ci = W;
       j.ldci = b;
@@ -426,7 +719,7 @@ int stbta_pobtasi_ex(const double* Ld, const double* Ll, const double* La, const
       TileJob j = job(Xd + i * bb, b, b, b, 1.0);
       j.lower = 1;
       j.mirror = 1;
-      j.p[j.nprod++] = prod(ws.T3, b, 0, W, b, 1, b, 1.0, 1);
+      j.p[j.nprod++] = prod(ws.T3[0], b, 0, W, b, 1, b, 1.0, 1);
       if ((e = launch_job(j, st))) return e;
     }
   }
