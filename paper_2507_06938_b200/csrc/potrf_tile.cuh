@@ -5,14 +5,9 @@
 // one tile, its log-det contribution (bta.py:238-246), and the TRSM
 // X := X L^-T (bta.py:213-219, scipy solve_triangular).
 //
-// Factorization: blocked right-looking on 32-wide sub-blocks in shared memory.
-//   kb = 0..3:  warp 0 factors L_kk in registers (one row per lane) and
-//               inverts it (one column per lane, loop form) -> W_kk;
-//               all warps: L_ik = A_ik W_kk^T (i > kb), then the trailing
-//               update A_ij -= L_ik L_jk^T, as interleaved 8x8 DMMA fragments.
-// Output: L (tile), the four W_kk^T blocks (the TRSM tasks' diagonal
-// inverses) and sum log diag L.  The code is kept compact (loops, not full
-// unrolling) because the persistent kernel's instruction footprint matters.
+// Factorization: blocked right-looking on 32-wide sub-blocks in shared memory
+// with a one-block look-ahead (see potrf_tile_smem).  Output: L (tile), the
+// four W_kk^T blocks (the TRSM tasks' diagonal inverses) and sum log diag L.
 #pragma once
 
 #include "common.cuh"
@@ -21,7 +16,7 @@ namespace stbta {
 
 constexpr int PT_LD = 129;   // row stride of the tile in shared memory
 constexpr int PT_WLD = 33;   // row stride of 32x32 blocks in shared memory
-constexpr int PT_SMEM_DOUBLES = 128 * PT_LD + 4 * 32 * PT_WLD + 128;
+constexpr int PT_SMEM_DOUBLES = 128 * PT_LD + 4 * 32 * PT_WLD + 192;
 
 // 8x8 DMMA fragments of up to U independent output tiles, interleaved so the
 // accumulator chains overlap: c[u] += sum_k A(m_u + g, k) * B(k, n_u + g').
@@ -110,15 +105,116 @@ STBTA_DEV unsigned long long pt_timer() {
   return t;
 }
 
+// Warp-level pieces of the tile Cholesky (one warp each; lane = row or column).
+
+// 1/sqrt(d) for d > 0: hardware approximation + two Newton steps (about 1 ulp;
+// avoids the library rsqrt's special-case paths, which are unrolled 32x in
+// factor32 and would blow up its instruction footprint).
+STBTA_DEV double rsqrt_nr(double d) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
+  const double h = 0.5 * d;
+  y = y * fma(-h * y, y, 1.5);
+  y = y * fma(-h * y, y, 1.5);
+  return y;
+}
+
+STBTA_DEV void named_bar_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// One warp's share of the tall factorization of column block kb (rows
+// [k0, 128) of the 32 columns [k0, k0+32)), right-looking column by column:
+//   role 0: the diagonal block, lane = row (factor; 1/L_jj to dinv, log-det)
+//   role 1: a 32-row block below it, lane = row (X := X L_kk^-T, i.e. the TRSM)
+//   role 2: identity rows, lane = row: the result is e_lane L_kk^-T, which is
+//           row `lane` of W_kk^T -- the diagonal-block inverse for the TRSM
+//           tasks, at no extra latency.
+// All roles run the same column step; the pivot column of the diagonal block
+// is broadcast through smem (colbuf, 64 doubles) under a named barrier over
+// the `nthr` factor threads.  Returns false on a non-positive pivot.
+STBTA_DEV bool factor_col32(double* T, int k0, int row0, int role, double* WTb, double* colbuf,
+                            double* dinv, double* ld_acc, int nthr) {
+  const int lane = threadIdx.x & 31;
+  double r[32];
+  if (role == 2) {
+#pragma unroll
+    for (int c = 0; c < 32; ++c) r[c] = (c == lane) ? 1.0 : 0.0;
+  } else {
+    const double* src = T + (row0 + lane) * PT_LD + k0;
+#pragma unroll
+    for (int c = 0; c < 32; ++c) r[c] = (role == 1 || c <= lane) ? src[c] : 0.0;
+  }
+  bool ok = true;
+  double mydiag = 1.0;
+#pragma unroll 32
+  for (int j = 0; j < 32; ++j) {
+    double* cb = colbuf + (j & 1) * 32;
+    if (role == 0) cb[lane] = r[j];  // unscaled column j of the diagonal block
+    named_bar_sync(1, nthr);
+    const double d = cb[j];
+    const double rs = rsqrt_nr(d);
+    const double lj = r[j] * rs;  // L[row][j] (= sqrt(d) on the diagonal)
+    if (role == 0) {
+      ok = ok && (d > 0.0);
+      if (lane == j) {
+        dinv[j] = rs;
+        mydiag = lj;
+      }
+    }
+    r[j] = lj;
+    const double t = lj * rs;
+#pragma unroll 32
+    for (int c = j + 1; c < 32; ++c) r[c] = fma(-t, cb[c], r[c]);  // L[c][j] = cb[c] * rs
+  }
+  if (role == 2) {
+#pragma unroll
+    for (int c = 0; c < 32; ++c) WTb[lane * PT_WLD + c] = r[c];
+  } else {
+    double* dst = T + (row0 + lane) * PT_LD + k0;
+#pragma unroll
+    for (int c = 0; c < 32; ++c)
+      if (role == 1 || c <= lane) dst[c] = r[c];
+  }
+  if (role == 0) *ld_acc += log(mydiag);
+  return role != 0 || __all_sync(0xffffffffu, ok);
+}
+
+// 32x32 block (br, bc) -= L_{br,kc} L_{bc,kc}^T over the 32 columns at kc, by
+// 64 threads (id in [0, 64)).
+STBTA_DEV void upd_blk32(double* T, int br, int bc, int kc, int id) {
+  double acc[4][4];
+  zero4x4(acc);
+  mma32_blk<32, true>(acc, T + br * 32 * PT_LD + kc, PT_LD, T + bc * 32 * PT_LD + kc, PT_LD, id);
+  const int tr = id & 7, tc = id >> 3;
+  double* d = T + br * 32 * PT_LD + bc * 32;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) d[(tr + 8 * i) * PT_LD + tc + 8 * j] -= acc[i][j];
+}
+
 // Returns 0 on success, 1 when a pivot is not positive (or NaN).
 // T: tile in shared memory (ld PT_LD), lower part valid on entry.
 // On exit: T lower = L; WT[kb] (32 x 32, ld PT_WLD) = (W_kk)^T, i.e.
 // WT[kb][c][i] = W_kk[i][c]; *logdet = sum log diag(L) (fixed order).
-// ph (optional, thread 0): ns of {factor+inverse, trsm, update}.
+//
+// Blocked right-looking Cholesky on 32-wide column blocks with a one-block
+// look-ahead, so only the pivot chain is serial:
+//   phase A (kb): warps 0..4-kb factor column block kb as one tall panel
+//                 (diagonal block, the blocks below = TRSM, identity rows =
+//                 W_kk^T); the other warps, in pairs, apply column block kb-1
+//                 to the trailing blocks right of column block kb+1.
+//   phase C (kb): column block kb+1 -= L_{.,kb} L_{kb+1,kb}^T (64 threads per
+//                 32x32 block), which the next tall panel needs.
+// ph (optional, thread 0): ns of {A, C}.  NT must be 256.
 template <int NT>
 STBTA_DEV int potrf_tile_smem(double* T, double* WT, double* scratch, double* logdet_out,
                               int* s_fail, unsigned long long* ph = nullptr) {
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  static_assert(NT == 256, "potrf_tile_smem is laid out for 8 warps");
+  const int tid = threadIdx.x, warp = tid >> 5;
+  double* dinv = scratch;          // 128: 1 / L_ii
+  double* colbuf = scratch + 128;  // 64: pivot column broadcast
   double ld_acc = 0.0;
   unsigned long long tp = (ph && tid == 0) ? pt_timer() : 0;
   auto stamp = [&](int k) {
@@ -132,105 +228,44 @@ STBTA_DEV int potrf_tile_smem(double* T, double* WT, double* scratch, double* lo
 #pragma unroll 1
   for (int kb = 0; kb < 4; ++kb) {
     const int k0 = kb * 32;
-    if (warp == 0) {
-      // ---- factor the 32x32 diagonal block, lane = row (registers)
-      double r[32];
-#pragma unroll
-      for (int c = 0; c < 32; ++c) r[c] = (c <= lane) ? T[(k0 + lane) * PT_LD + k0 + c] : 0.0;
-      bool ok = true;
-      double* colbuf = scratch + 32;  // 2 x 32, double-buffered column of the pivot step
-#pragma unroll 32
-      for (int j = 0; j < 32; ++j) {
-        double* cb = colbuf + (j & 1) * 32;
-        cb[lane] = r[j];  // unscaled column j (this lane's row)
-        __syncwarp();
-        const double d = cb[j];
-        ok = ok && (d > 0.0);
-        const double rs = rsqrt(d);
-        const double lj = (lane == j) ? d * rs : r[j] * rs;  // L[lane][j]
-        r[j] = lj;
-        const double t = lj * rs;
-        // entries above this lane's diagonal are never read: update them freely
-#pragma unroll 32
-        for (int c = j + 1; c < 32; ++c) r[c] = fma(-t, cb[c], r[c]);  // L[c][j] = cb[c] * rs
+    const int nfw = 5 - kb;  // factor warps: diagonal, 3-kb row blocks, identity
+    // ---- phase A
+    if (warp < nfw) {
+      const int role = warp == 0 ? 0 : (warp == nfw - 1 ? 2 : 1);
+      if (!factor_col32(T, k0, k0 + 32 * warp, role, WT + kb * 32 * PT_WLD, colbuf, dinv + k0,
+                        &ld_acc, 32 * nfw) &&
+          tid == 0)
+        *s_fail = 1;
+    } else if (kb > 0) {
+      // blocks (br, bc), kb+1 <= bc <= br < 4, -= L_{br,kb-1} L_{bc,kb-1}^T
+      const int grp = (warp - nfw) >> 1, ngrp = (8 - nfw) >> 1;
+      const int id = tid - 32 * nfw - 64 * grp;
+      if (grp < ngrp) {
+        int idx = 0;
+#pragma unroll 1
+        for (int bc = kb + 1; bc < 4; ++bc)
+#pragma unroll 1
+          for (int br = bc; br < 4; ++br)
+            if (idx++ % ngrp == grp) upd_blk32(T, br, bc, k0 - 32, id);
       }
-      if (!ok && lane == 0) *s_fail = 1;
-      stamp(3);
-#pragma unroll
-      for (int c = 0; c < 32; ++c)
-        if (c <= lane) T[(k0 + lane) * PT_LD + k0 + c] = r[c];
-      __syncwarp();
-      const double dl = T[(k0 + lane) * PT_LD + k0 + lane];
-      ld_acc += log(dl);
-      scratch[lane] = 1.0 / dl;
-      __syncwarp();
-      // ---- W_kk = L_kk^-1, lane = column c: w[i] for i >= c (registers)
-      double w[32];
-#pragma unroll
-      for (int i = 0; i < 32; ++i) w[i] = (i == lane) ? 1.0 : 0.0;
-#pragma unroll 32
-      for (int k = 0; k < 32; ++k) {
-        w[k] *= scratch[k];
-#pragma unroll 32
-        for (int i = k + 1; i < 32; ++i) w[i] = fma(-T[(k0 + i) * PT_LD + k0 + k], w[k], w[i]);
-      }
-      double* wc = WT + kb * 32 * PT_WLD + lane * PT_WLD;  // WT[kb][c][i] = W[i][c]
-#pragma unroll
-      for (int i = 0; i < 32; ++i) wc[i] = w[i];
     }
     __syncthreads();
     stamp(0);
     if (*s_fail) return 1;
-    const int rem = 96 - k0;  // rows below the diagonal block
-    if (rem == 0) break;
-    // ---- TRSM: L_ik = A_ik W_kk^T for rows [k0+32, 128) (32x32 blocks, 64 threads each)
+    if (kb == 3) break;
+    // ---- phase C: blocks (br, kb+1), br = kb+1..3, from column block kb
     {
-      const int nblk = rem / 32;
       const int blk = tid >> 6, id = tid & 63;
-      double acc[4][4];
-      zero4x4(acc);
-      if (blk < nblk)
-        mma32_blk<32, false>(acc, T + (k0 + 32 + blk * 32) * PT_LD + k0, PT_LD,
-                             WT + kb * 32 * PT_WLD, PT_WLD, id);
-      __syncthreads();
-      if (blk < nblk) {
-        const int tr = id & 7, tc = id >> 3;
-        double* d = T + (k0 + 32 + blk * 32) * PT_LD + k0;
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-          for (int j = 0; j < 4; ++j) d[(tr + 8 * i) * PT_LD + tc + 8 * j] = acc[i][j];
-      }
+      if (blk < 3 - kb) upd_blk32(T, kb + 1 + blk, kb + 1, k0, id);
     }
     __syncthreads();
     stamp(1);
-    // ---- trailing update: A_rc -= L_r L_c^T on lower 32x32 blocks (64 threads each)
-    {
-      const int nb = rem / 32;
-      const int nblk = nb * (nb + 1) / 2;
-      const double* base = T + (k0 + 32) * PT_LD + k0;
-#pragma unroll 1
-      for (int blk = tid >> 6; blk < nblk; blk += NT / 64) {
-        int br, bc;
-        tri_decode(blk, &br, &bc);
-        const int id = tid & 63, tr = id & 7, tc = id >> 3;
-        double acc[4][4];
-        zero4x4(acc);
-        mma32_blk<32, true>(acc, base + br * 32 * PT_LD, PT_LD, base + bc * 32 * PT_LD, PT_LD, id);
-        double* d = T + (k0 + 32 + br * 32) * PT_LD + k0 + 32 + bc * 32;
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-          for (int j = 0; j < 4; ++j) d[(tr + 8 * i) * PT_LD + tc + 8 * j] -= acc[i][j];
-      }
-    }
-    __syncthreads();
-    stamp(2);
   }
   if (warp == 0) {
     const double s = warp_sum(ld_acc);
-    if (lane == 0) *logdet_out = s;
+    if ((tid & 31) == 0) *logdet_out = s;
   }
+  __syncthreads();
   return 0;
 }
 

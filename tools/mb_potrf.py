@@ -14,8 +14,8 @@ for grid in (1, 148):
     lib.stbta_debug_potrf_bench(_lib.ptr(A), _lib.ptr(out), reps, grid, _lib.ptr(ph), st)
     torch.cuda.synchronize()
     p = ph.cpu().tolist()
-    print(f"grid={grid}: {p[5]/reps/1e3:.2f} us/potrf  phases us: factor {p[3]/reps/1e3:.2f} inv+ {p[0]/reps/1e3:.2f} trsm {p[1]/reps/1e3:.2f} "
-          f"update {p[2]/reps/1e3:.2f}  logdet {out[0].item():.12f} ref {2*torch.log(torch.diagonal(ref)).sum().item()/2:.12f}"
+    print(f"grid={grid}: {p[5]/reps/1e3:.2f} us/potrf  phases us: A(tall factor|upd) {p[0]/reps/1e3:.2f} C(next column) {p[1]/reps/1e3:.2f} "
+          f"logdet {out[0].item():.12f} ref {2*torch.log(torch.diagonal(ref)).sum().item()/2:.12f}"
           f" W[127,0] {out[1].item():.6e} ref {torch.linalg.inv(ref)[127,0].item():.6e}", flush=True)
 cyc = torch.zeros(1, dtype=torch.int64, device=dev)
 for which, name in ((0, "DMMA"), (1, "DFMA")):

@@ -31,4 +31,4 @@ for k, name in enumerate(["POTRF", "TRSM", "UPDATE", "STRIP"]):
     c, w, e = p[3*k:3*k+3]
     if c:
         print(f"{name:7s} n={c:8d} wait {w/c/1e3:9.2f} us/task exec {e/c/1e3:9.2f} us/task  total exec {e/1e6:9.2f} ms wait {w/1e6:9.2f} ms")
-print("POTRF phases (us per task): factor+inv %.2f trsm %.2f update %.2f - %.2f load/store %.2f pre %.2f" % tuple(x/1e3/max(p[0],1) for x in p[12:18]))
+print("POTRF phases (us per task): A %.2f C %.2f - %.2f - %.2f store %.2f load %.2f" % tuple(x/1e3/max(p[0],1) for x in p[12:18]))
