@@ -399,8 +399,8 @@ def main():
             fac = bta.factorize(m, use_arrow=True)                 # bta.py:177
             bta.logdet(fac)                                        # bta.py:238
             xs = bta.solve(fac, host_rhs)                          # bta.py:305 (host in/out)
-            sel = bta.selected_invert(fac)                         # bta.py:310
-            sel.numpy(out=host_out)                                # D2H of the inverse
+            sel = bta.selected_invert(fac, out=host_out)           # bta.py:310, streamed to host
+            sel.numpy(out=host_out)                                # waits for the D2H stream
             return xs
 
         e2e_step()
@@ -421,7 +421,9 @@ def main():
         e2e = {"value": world * step_flops * e2e_steps / t_e2e / 1e12, "unit": UNIT,
                "h2d_bytes_per_step": nbytes + 8 * (n * b + a),
                "d2h_bytes_per_step": nbytes + 8 * (n * b + a) + 8 + 4,
-               "steps": e2e_steps, "timing": "host wall clock around synchronous API calls"}
+               "steps": e2e_steps, "timing": "host wall clock around synchronous API calls",
+               "overlap": "H2D in time-block chunks overlapped with POBTAF (per-block ready flags); "
+                          "inverse D2H block by block overlapped with POBTASI (completion counters)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:

@@ -93,6 +93,38 @@ int stbta_pobtasi_ex(const double* Ld, const double* Ll, const double* La, const
                      int has_arrow, int nstart, void* workspace, size_t workspace_bytes,
                      void* stream);
 
+/* ----------------------------------------- pipelined host <-> device I/O --
+ * The reference keeps matrices in host memory (numpy); a host-resident BTA
+ * matrix used through the device path (BTAMatrix(host data) -> factorize ->
+ * solve -> selected_invert -> host inverse, bta.py:50-359) is moved in time-
+ * block chunks overlapped with the compute instead of before / after it.
+ * Requires the driver's stream memory operations (cuStreamWriteValue32 /
+ * cuStreamWaitValue32, resolved at run time):
+ *   stbta_stream_memops_supported: 1 when available (else the entry points
+ *     below return cudaErrorNotSupported).
+ *   stbta_upload_blocks: copy the flat buffer src_host (PINNED host memory)
+ *     to dst on `stream` in chunks {diag[t], lower[t], arrow[t]} (the tip with
+ *     the first chunk), writing ready[t] = epoch after chunk t has landed.
+ *   stbta_pobtaf_ready: stbta_pobtaf whose task graph starts at once and waits
+ *     per task for ready[chunk] - epoch >= 0 of the block it touches; `stream`
+ *     must NOT wait for the upload stream (that is the point), and the upload
+ *     must not wait for `stream` after this launch.
+ *   stbta_pobtasi_stream_out: stbta_pobtasi on `stream`, plus block-wise
+ *     device->host copies of the inverse into host_out (PINNED, flat layout)
+ *     on copy_stream, each gated on the recursion's completion counter of that
+ *     block; record an event on copy_stream to know when host_out is final. */
+int stbta_stream_memops_supported(void);
+/* Debug: *out (device u64) = %globaltimer (ns) when this point of `stream` runs. */
+int stbta_debug_globaltimer(unsigned long long* out, void* stream);
+int stbta_upload_blocks(double* dst, const double* src_host, int n, int b, int a, unsigned* ready,
+                        unsigned epoch, void* stream);
+int stbta_pobtaf_ready(double* data, int n, int b, int a, int use_arrow, double* logdet_out,
+                       int* info, const unsigned* ready, unsigned epoch, void* workspace,
+                       size_t workspace_bytes, void* stream);
+int stbta_pobtasi_stream_out(const double* factor, double* inv, double* host_out, int n, int b,
+                             int a, int has_arrow, void* workspace, size_t workspace_bytes,
+                             void* stream, void* copy_stream);
+
 /* ------------------------------------------------------ Q assembly / f_obj --
  * stbta_assemble: write the theta-dependent values of a precision matrix into
  * a BTA buffer of nstore elements, zero everywhere else.  Replaces the value

@@ -55,6 +55,17 @@ _SIGNATURES = {
         c_int,
         [c_int, c_int, c_int, c_int, c_int, c_dbl, c_vp, c_ll, c_vp, c_ll, c_dbl, c_vp, c_ll, c_vp],
     ),
+    "stbta_stream_memops_supported": (c_int, []),
+    "stbta_debug_globaltimer": (c_int, [c_vp, c_vp]),
+    "stbta_upload_blocks": (c_int, [c_vp, c_vp, c_int, c_int, c_int, c_vp, ctypes.c_uint, c_vp]),
+    "stbta_pobtaf_ready": (
+        c_int,
+        [c_vp, c_int, c_int, c_int, c_int, c_vp, c_vp, c_vp, ctypes.c_uint, c_vp, c_size, c_vp],
+    ),
+    "stbta_pobtasi_stream_out": (
+        c_int,
+        [c_vp, c_vp, c_vp, c_int, c_int, c_int, c_int, c_vp, c_size, c_vp, c_vp],
+    ),
     "stbta_launch_count": (c_ll, []),
     "stbta_debug_set_profile": (None, [c_vp]),
     "stbta_debug_potrf_bench": (c_int, [c_vp, c_vp, c_int, c_int, c_vp, c_vp]),

@@ -51,6 +51,32 @@ class OpCounter:
         self.flops += float(units)
 
 
+_SIDE_STREAMS = {}
+
+
+def _side_stream(dev, role):
+    """One cached side stream per (device, role) for the pipelined copies."""
+    dev = torch.device(dev)
+    key = (dev.index if dev.index is not None else torch.cuda.current_device(), role)
+    st = _SIDE_STREAMS.get(key)
+    if st is None:
+        st = _SIDE_STREAMS[key] = torch.cuda.Stream(device=key[0])
+    return st
+
+
+_MEMOPS = None
+
+
+def _memops_supported():
+    global _MEMOPS
+    if _MEMOPS is None:
+        try:
+            _MEMOPS = bool(torch.cuda.is_available() and _lib.load().stbta_stream_memops_supported())
+        except Exception:
+            _MEMOPS = False
+    return _MEMOPS
+
+
 def default_device():
     _lib.load()
     return torch.device("cuda", torch.cuda.current_device())
@@ -78,6 +104,8 @@ class BTAMatrix:
             )
         self.n_blocks, self.block_size, self.arrow_size = n_blocks, block_size, arrow_size
         total = _storage_elems(n_blocks, block_size, arrow_size)
+        self._upload = None      # (ready flags, done event, host source) of a pipelined upload
+        self._host_copy = None   # (pinned host tensor, done event) of a streamed-out result
         if data is None:
             dev = torch.device(device) if device is not None else default_device()
             data = torch.zeros(total, dtype=torch.float64, device=dev)
@@ -86,25 +114,73 @@ class BTAMatrix:
                 raise ValueError("data must be a float64 tensor")
             if data.numel() != total or data.dim() != 1 or not data.is_contiguous():
                 raise ValueError(f"data buffer must have {total} entries")
-            if not data.is_cuda:  # host tensor (pinned for an async upload): copied
+            if not data.is_cuda:  # host tensor: copied (pipelined per time block when pinned)
                 dev = torch.device(device) if device is not None else default_device()
-                data = data.to(dev, non_blocking=data.is_pinned())
+                if data.is_pinned() and _memops_supported():
+                    data = self._start_upload(data, dev)
+                else:
+                    data = data.to(dev, non_blocking=data.is_pinned())
         else:
             arr = np.asarray(data, dtype=np.float64)
             if arr.shape != (total,):
                 raise ValueError(f"data buffer must have {total} entries")
             dev = torch.device(device) if device is not None else default_device()
             data = torch.from_numpy(np.ascontiguousarray(arr)).to(dev)
-        self.data = data
-        n, b, a = n_blocks, block_size, arrow_size
-        e0 = n * b * b
-        e1 = e0 + (n - 1) * b * b
-        e2 = e1 + n * a * b
-        self.diag = data[:e0].view(n, b, b)
-        self.lower = data[e0:e1].view(n - 1, b, b)
-        self.arrow = data[e1:e2].view(n, a, b)
-        self.tip = data[e2:].view(a, a)
+        self._data = data
         self._scatter_source = None
+
+    def _start_upload(self, host, dev):
+        """Chunked H2D copy on a side stream; per-block flags let POBTAF start
+        before the upload has finished (stbta_upload_blocks / stbta_pobtaf_ready)."""
+        lib = _lib.load()
+        n, b, a = self.n_blocks, self.block_size, self.arrow_size
+        with torch.cuda.device(dev):
+            cur = torch.cuda.current_stream()
+            dst = torch.empty(host.numel(), dtype=torch.float64, device=dev)
+            flags = torch.zeros(n, dtype=torch.int32, device=dev)
+            up = _side_stream(dev, "upload")
+            up.wait_stream(cur)  # allocation + flag zeroing precede the copies
+            _lib.check(
+                lib.stbta_upload_blocks(_lib.ptr(dst), host.data_ptr(), n, b, a, _lib.ptr(flags), 1,
+                                        up.cuda_stream),
+                "stbta_upload_blocks",
+            )
+            done = torch.cuda.Event()
+            done.record(up)
+            dst.record_stream(up)
+            flags.record_stream(up)
+        self._upload = (flags, done, host)
+        return dst
+
+    @property
+    def data(self):
+        """The flat device buffer; waits (stream-ordered) for a pending upload."""
+        if self._upload is not None:
+            torch.cuda.current_stream(self._data.device).wait_event(self._upload[1])
+        return self._data
+
+    @property
+    def diag(self):
+        n, b = self.n_blocks, self.block_size
+        return self.data[: n * b * b].view(n, b, b)
+
+    @property
+    def lower(self):
+        n, b = self.n_blocks, self.block_size
+        e0 = n * b * b
+        return self.data[e0 : e0 + (n - 1) * b * b].view(n - 1, b, b)
+
+    @property
+    def arrow(self):
+        n, b, a = self.n_blocks, self.block_size, self.arrow_size
+        e1 = (2 * n - 1) * b * b
+        return self.data[e1 : e1 + n * a * b].view(n, a, b)
+
+    @property
+    def tip(self):
+        n, b, a = self.n_blocks, self.block_size, self.arrow_size
+        e2 = (2 * n - 1) * b * b + n * a * b
+        return self.data[e2:].view(a, a)
 
     @property
     def dim(self):
@@ -112,7 +188,7 @@ class BTAMatrix:
 
     @property
     def device(self):
-        return self.data.device
+        return self._data.device
 
     def copy(self):
         return BTAMatrix(self.n_blocks, self.block_size, self.arrow_size, self.data.clone())
@@ -124,7 +200,11 @@ class BTAMatrix:
 
     def numpy(self, out=None):
         """Host copy of the flat buffer; ``out`` may be a (pinned) CPU float64
-        tensor of the same size that receives the copy."""
+        tensor of the same size that receives the copy (when it is the buffer
+        this matrix was already streamed into, only the copy is awaited)."""
+        if self._host_copy is not None and out is self._host_copy[0]:
+            self._host_copy[1].synchronize()
+            return out.numpy()
         if out is not None:
             out.copy_(self.data)
             return out.numpy()
@@ -221,6 +301,17 @@ def factorize_async(matrix, use_arrow, stream=None):
     out = torch.zeros(2, dtype=torch.float64, device=dev)
     info = torch.zeros(1, dtype=torch.int32, device=dev)
     matrix._scatter_source = None
+    if matrix._upload is not None and not matrix._upload[1].query() and stream is None:
+        # the upload is still in flight: the task graph waits per time block
+        flags = matrix._upload[0]
+        _lib.check(
+            lib.stbta_pobtaf_ready(
+                _lib.ptr(matrix._data), n, b, a, int(bool(use_arrow)), _lib.ptr(out),
+                _lib.ptr(info), _lib.ptr(flags), 1, _lib.ptr(ws), ws.numel(), _lib.stream_ptr(None),
+            ),
+            "stbta_pobtaf_ready",
+        )
+        return out, info
     _lib.check(
         lib.stbta_pobtaf(
             _lib.ptr(matrix.data), n, b, a, int(bool(use_arrow)), _lib.ptr(out), _lib.ptr(info),
@@ -329,21 +420,44 @@ def solve(factor, rhs, counter=None):
     return _solve_api(factor, rhs, 0, counter)
 
 
-def selected_invert(factor, counter=None, stream=None):
-    """Pattern entries of M^-1 as a new BTAMatrix (reference bta.py:310-359)."""
+def selected_invert(factor, counter=None, stream=None, out=None):
+    """Pattern entries of M^-1 as a new BTAMatrix (reference bta.py:310-359).
+
+    ``out``: optional pinned CPU float64 tensor of the storage size; the
+    inverse then also streams into it block by block while the recursion
+    runs (``inv.numpy(out=out)`` waits for the copy only).
+    """
     lib = _lib.load()
     m = factor.matrix
     n, b, a = m.n_blocks, m.block_size, m.arrow_size
     with torch.cuda.device(m.device):
         inv = BTAMatrix(n, b, a, torch.empty_like(m.data))
         ws = _workspace(lib.stbta_pobtasi_workspace_bytes(n, b, a), m.device)
-        _lib.check(
-            lib.stbta_pobtasi(
-                _lib.ptr(m.data), _lib.ptr(inv.data), n, b, a, int(bool(factor.has_arrow)),
-                _lib.ptr(ws), ws.numel(), _lib.stream_ptr(stream),
-            ),
-            "stbta_pobtasi",
-        )
+        if (out is not None and isinstance(out, torch.Tensor) and not out.is_cuda and out.is_pinned()
+                and out.dtype == torch.float64 and out.numel() == inv._data.numel()
+                and out.is_contiguous() and stream is None):
+            cs = _side_stream(m.device, "download")
+            _lib.check(
+                lib.stbta_pobtasi_stream_out(
+                    _lib.ptr(m.data), _lib.ptr(inv.data), out.data_ptr(), n, b, a,
+                    int(bool(factor.has_arrow)), _lib.ptr(ws), ws.numel(), _lib.stream_ptr(None),
+                    cs.cuda_stream,
+                ),
+                "stbta_pobtasi_stream_out",
+            )
+            done = torch.cuda.Event()
+            done.record(cs)
+            inv._data.record_stream(cs)
+            ws.record_stream(cs)
+            inv._host_copy = (out, done)
+        else:
+            _lib.check(
+                lib.stbta_pobtasi(
+                    _lib.ptr(m.data), _lib.ptr(inv.data), n, b, a, int(bool(factor.has_arrow)),
+                    _lib.ptr(ws), ws.numel(), _lib.stream_ptr(stream),
+                ),
+                "stbta_pobtasi",
+            )
     if counter is not None:
         for _ in range(n):
             counter.charge(b**3)

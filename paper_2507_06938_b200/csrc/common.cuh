@@ -37,6 +37,11 @@ inline void attr_mark(std::atomic<unsigned long long>& mask) {
 // Host-side count of kernel launches issued by the library (bench.py's
 // gpu_launches; read with stbta_launch_count()).
 void count_launch();
+// Stream-ordered zero fill by an SM kernel.  cudaMemsetAsync may be carried
+// out by a copy engine and then queues behind unrelated bulk host<->device
+// copies of other streams (the pipelined uploads), stalling the compute
+// stream; a kernel does not.
+int zero_async(void* p, size_t bytes, cudaStream_t st);
 // Debug profile buffer set by stbta_debug_set_profile (nullptr: disabled).
 unsigned long long* debug_profile();
 

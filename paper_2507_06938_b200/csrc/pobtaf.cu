@@ -68,7 +68,31 @@ struct DagWs {
   int* role;     // first CTA to arrive becomes the panel (POTRF) worker
   int G;
   unsigned long long* prof;  // optional: per task type {count, wait ns, exec ns}
+  const unsigned* ready;     // optional: per time block upload flags (stbta_upload_blocks)
+  unsigned epoch;            // ... a block is resident once ready[t] - epoch >= 0
 };
+
+// Upload chunk holding tile (R, C): chunk t = {diag[t], lower[t], arrow[t]},
+// the tip travels with the first chunk (every block's arrow updates it).
+STBTA_DEV int tile_chunk(const Band& g, int C) {
+  return C < g.n * g.nbt ? C / g.nbt : 0;
+}
+
+// Wait until the chunk of tile column C is resident (pipelined host upload).
+STBTA_DEV bool wait_resident(const Band& g, const DagWs& ws, int C) {
+  if (ws.ready == nullptr) return true;
+  const unsigned* p = ws.ready + tile_chunk(g, C);
+  int it = 0;
+  for (;;) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+    if ((int)(v - ws.epoch) >= 0) return true;
+    if (ld_volatile(ws.abort_flag)) return false;
+    // back off: many CTAs may poll the same flag while a chunk is in flight
+    __nanosleep(it < 4 ? 128 : 1024);
+    ++it;
+  }
+}
 
 STBTA_DEV unsigned long long gtimer() {
   unsigned long long t;
@@ -213,6 +237,15 @@ STBTA_DEV bool potrf_worker(const Band& g, const DagWs& ws, int* info, double* s
     if (tid == 0) { s_ok = 1; s_fail = 0; }
     __syncthreads();
     if (tid < NSTRIP && !spin_geq(counter(g, ws.ctr, s, tid, s), need(g, s, s), ws.abort_flag)) s_ok = 0;
+    if (tid == NSTRIP) {
+      const unsigned long long tw0 = ws.prof ? gtimer() : 0;
+      if (!wait_resident(g, ws, s)) s_ok = 0;
+      if (ws.prof) {
+        unsigned long long* tlp = ws.prof + PROF_TL + (long long)s * 12;
+        tlp[10] = tw0;
+        tlp[11] = gtimer();
+      }
+    }
     __syncthreads();
     if (!s_ok) return false;
     if (ws.prof != nullptr && tid == 0) t1 = gtimer();
@@ -341,6 +374,8 @@ __global__ void __launch_bounds__(DAG_NT, 1) pobtaf_dag_kernel(Band g, DagWs ws,
         else if (tid == NSTRIP) { p = counter(g, ws.ctr, tk.R, tk.q, tk.R); target = n_updates(g, tk.R, tk.R, s); }
       }
       if (p != nullptr && !spin_geq(p, target, ws.abort_flag)) s_ok = 0;
+      if (tid == 32 && !wait_resident(g, ws, tk.type == T_UPD ? tk.C : tk.type == T_STRIP ? tk.R : s))
+        s_ok = 0;
       __syncthreads();
       if (!s_ok) break;
     }
@@ -538,6 +573,8 @@ static size_t dag_ws(const Band& g, char* base, DagWs* o, size_t* zero_bytes) {
     o->W = reinterpret_cast<double*>(base + gs + cz + sl);
     o->G = G;
     o->prof = nullptr;
+    o->ready = nullptr;
+    o->epoch = 0;
   }
   if (zero_bytes) *zero_bytes = cz;
   return gs + cz + sl + wb;
@@ -580,9 +617,36 @@ int stbta_pobtaf(double* data, int n, int b, int a, int use_arrow, double* logde
                          workspace, workspace_bytes, stream);
 }
 
+static int pobtaf_impl(double* diag, double* lower, double* arrow, double* tip, int n, int b, int a,
+                       int ldb, int use_arrow, int nfact, double* logdet_out, int* info,
+                       const unsigned* ready, unsigned epoch, void* workspace,
+                       size_t workspace_bytes, void* stream);
+
 int stbta_pobtaf_ex(double* diag, double* lower, double* arrow, double* tip, int n, int b, int a,
                     int ldb, int use_arrow, int nfact, double* logdet_out, int* info,
                     void* workspace, size_t workspace_bytes, void* stream) {
+  return pobtaf_impl(diag, lower, arrow, tip, n, b, a, ldb, use_arrow, nfact, logdet_out, info,
+                     nullptr, 0u, workspace, workspace_bytes, stream);
+}
+
+int stbta_pobtaf_ready(double* data, int n, int b, int a, int use_arrow, double* logdet_out,
+                       int* info, const unsigned* ready, unsigned epoch, void* workspace,
+                       size_t workspace_bytes, void* stream) {
+  if (data == nullptr || ready == nullptr) return STBTA_EARG;
+  const long long bb = (long long)b * b;
+  double* lower = data + (long long)n * bb;
+  double* arrow = lower + (long long)(n - 1) * bb;
+  double* tip = arrow + (long long)n * a * b;
+  return pobtaf_impl(data, lower, arrow, tip, n, b, a, b, use_arrow, -1, logdet_out, info, ready,
+                     epoch, workspace, workspace_bytes, stream);
+}
+
+}  // extern "C"
+
+static int pobtaf_impl(double* diag, double* lower, double* arrow, double* tip, int n, int b, int a,
+                       int ldb, int use_arrow, int nfact, double* logdet_out, int* info,
+                       const unsigned* ready, unsigned epoch, void* workspace,
+                       size_t workspace_bytes, void* stream) {
   if (diag == nullptr || n < 1 || b < 1 || a < 0 || info == nullptr || nfact > n || ldb < b)
     return STBTA_EARG;
   if ((n > 1 && lower == nullptr) || (a > 0 && (arrow == nullptr || tip == nullptr)))
@@ -592,14 +656,16 @@ int stbta_pobtaf_ex(double* diag, double* lower, double* arrow, double* tip, int
   const double* regions[4] = {diag, lower, arrow, tip};
   const Band g = make_band(regions, n, b, a, use_arrow, nfact, ldb);
   if (g.SP == 0) {  // nothing to eliminate
-    int e = (int)cudaMemsetAsync(info, 0, sizeof(int), st);
-    if (!e && logdet_out) e = (int)cudaMemsetAsync(logdet_out, 0, sizeof(double), st);
+    int e = zero_async(info, sizeof(int), st);
+    if (!e && logdet_out) e = zero_async(logdet_out, sizeof(double), st);
     return e;
   }
   DagWs ws;
   size_t zbytes = 0;
   dag_ws(g, reinterpret_cast<char*>(workspace), &ws, &zbytes);
   ws.prof = debug_profile();
+  ws.ready = ready;
+  ws.epoch = epoch;
   static std::atomic<unsigned long long> attr_mask{0};  // per device
   if (attr_pending(attr_mask)) {
     int e = (int)cudaFuncSetAttribute(pobtaf_dag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -607,9 +673,9 @@ int stbta_pobtaf_ex(double* diag, double* lower, double* arrow, double* tip, int
     if (e) return e;
     attr_mark(attr_mask);
   }
-  int e = (int)cudaMemsetAsync(info, 0, sizeof(int), st);
+  int e = zero_async(info, sizeof(int), st);
   if (e) return e;
-  if ((e = (int)cudaMemsetAsync(ws.ctr, 0, zbytes, st))) return e;
+  if ((e = zero_async(ws.ctr, zbytes, st))) return e;
   dag_setup_kernel<<<1, 1024, 0, st>>>(g, ws);
   count_launch();
   if ((e = (int)cudaGetLastError())) return e;
@@ -623,6 +689,8 @@ int stbta_pobtaf_ex(double* diag, double* lower, double* arrow, double* tip, int
   }
   return 0;
 }
+
+extern "C" {
 
 int stbta_dgemm(int ta, int tb, int M, int N, int K, double alpha, const double* A, long long lda,
                 const double* B, long long ldb, double beta, double* C, long long ldc,

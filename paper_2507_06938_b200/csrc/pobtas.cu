@@ -431,7 +431,7 @@ static int run_sweeps(SweepArgs p, int mode, const PobtasWs& ws, cudaStream_t st
   count_launch();
   if ((e = (int)cudaGetLastError())) return e;
   if (mode == 0 || mode == 1) {
-    if ((e = (int)cudaMemsetAsync(p.flags, 0, fbytes, st))) return e;
+    if ((e = zero_async(p.flags, fbytes, st))) return e;
     if (p.ncols == 1) sweep_kernel<true, 1><<<p.ntile, PS_NT, smem, st>>>(p);
     else sweep_kernel<true, NR><<<p.ntile, PS_NT, smem, st>>>(p);
     count_launch();
@@ -448,7 +448,7 @@ static int run_sweeps(SweepArgs p, int mode, const PobtasWs& ws, cudaStream_t st
       count_launch();
       if ((e = (int)cudaGetLastError())) return e;
     }
-    if ((e = (int)cudaMemsetAsync(p.flags, 0, fbytes, st))) return e;
+    if ((e = zero_async(p.flags, fbytes, st))) return e;
     if (p.ncols == 1) sweep_kernel<false, 1><<<p.ntile, PS_NT, smem, st>>>(p);
     else sweep_kernel<false, NR><<<p.ntile, PS_NT, smem, st>>>(p);
     count_launch();

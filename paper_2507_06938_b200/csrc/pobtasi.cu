@@ -24,6 +24,7 @@
 #include "potrf_tile.cuh"
 #include "stbta_internal.cuh"
 #include "tile_mma.cuh"
+#include "memops.cuh"
 
 namespace stbta {
 
@@ -463,7 +464,9 @@ __global__ void __launch_bounds__(SI_NT, 1) sinv_persistent_kernel(SiParams P) {
     __syncthreads();
     if (threadIdx.x == 0) {
       int* c = ctr_slot(P, i, kinfo & 0xff);
-      __threadfence();
+      // finished X blocks may be read by a copy engine (stbta_pobtasi_stream_out)
+      if (i < 0 || (kinfo & 0xff) == K_XII) __threadfence_system();
+      else __threadfence();
       atomicAdd(c + tr, 1);
       atomicAdd(c + P.cm + tc, 1);
       atomicAdd(c + 2 * P.cm, 1);
@@ -575,10 +578,78 @@ int stbta_pobtasi(const double* factor, double* inv, int n, int b, int a, int ha
                           workspace, workspace_bytes, stream);
 }
 
+static int pobtasi_impl(const double* Ld, const double* Ll, const double* La, const double* Lt,
+                        double* Xd, double* Xl, double* Xa, double* Xt, int n, int b, int a,
+                        int has_arrow, int nstart, void* workspace, size_t workspace_bytes,
+                        void* stream, cudaEvent_t ctr_ready, int* persistent);
+
 int stbta_pobtasi_ex(const double* Ld, const double* Ll, const double* La, const double* Lt,
                      double* Xd, double* Xl, double* Xa, double* Xt, int n, int b, int a,
                      int has_arrow, int nstart, void* workspace, size_t workspace_bytes,
                      void* stream) {
+  return pobtasi_impl(Ld, Ll, La, Lt, Xd, Xl, Xa, Xt, n, b, a, has_arrow, nstart, workspace,
+                      workspace_bytes, stream, nullptr, nullptr);
+}
+
+int stbta_pobtasi_stream_out(const double* factor, double* inv, double* host_out, int n, int b,
+                             int a, int has_arrow, void* workspace, size_t workspace_bytes,
+                             void* stream, void* copy_stream) {
+  if (factor == nullptr || inv == nullptr || host_out == nullptr || n < 1 || b < 1 || a < 0)
+    return STBTA_EARG;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  cudaStream_t cs = reinterpret_cast<cudaStream_t>(copy_stream);
+  const long long bb = (long long)b * b;
+  const long long o_low = (long long)n * bb, o_arr = o_low + (long long)(n - 1) * bb;
+  const long long o_tip = o_arr + (long long)n * a * b;
+  cudaEvent_t ev;
+  int e = (int)cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+  if (e) return e;
+  int persistent = 0;
+  e = pobtasi_impl(factor, factor + o_low, factor + o_arr, factor + o_tip, inv, inv + o_low,
+                   inv + o_arr, inv + o_tip, n, b, a, has_arrow, -1, workspace, workspace_bytes,
+                   stream, memops().ok ? ev : nullptr, &persistent);
+  if (e) {
+    cudaEventDestroy(ev);
+    return e;
+  }
+  auto d2h = [&](long long off, long long elems) {
+    return (int)cudaMemcpyAsync(host_out + off, inv + off, elems * sizeof(double),
+                                cudaMemcpyDeviceToHost, cs);
+  };
+  if (!persistent || !memops().ok) {  // whole buffer once the recursion is done
+    if (!(e = (int)cudaEventRecord(ev, st)) && !(e = (int)cudaStreamWaitEvent(cs, ev, 0)))
+      e = d2h(0, o_tip + (long long)a * a);
+    cudaEventDestroy(ev);
+    return e;
+  }
+  // counters of the persistent kernel (same layout as SiParams / ctr_slot)
+  PobtasiWs ws;
+  pobtasi_ws(n, b, a, reinterpret_cast<char*>(workspace), &ws);
+  const int ntb = (b + 127) / 128, tma = a <= 32 ? 1 : (a + 127) / 128, tnt = (a + 127) / 128;
+  const int cm = si_cm(b, a), cslot = 2 * cm + 1;
+  const int* ctr = ws.ctr + 4;
+  if ((e = (int)cudaStreamWaitEvent(cs, ev, 0))) return cudaEventDestroy(ev), e;
+  cudaEventDestroy(ev);
+  if (a > 0) {
+    if ((e = memops_wait_geq(cs, ctr + 2 * cm, (unsigned)(tma * tnt)))) return e;
+    if ((e = d2h(o_tip, (long long)a * a))) return e;
+  }
+  for (int i = n - 1; i >= 0; --i) {
+    const int* c = ctr + (long long)(1 + (long long)(n - 1 - i) * K_NKIND + K_XII) * cslot;
+    if ((e = memops_wait_geq(cs, c + 2 * cm, (unsigned)(ntb * (ntb + 1) / 2)))) return e;
+    if ((e = d2h((long long)i * bb, bb))) return e;
+    if (i < n - 1 && (e = d2h(o_low + (long long)i * bb, bb))) return e;
+    if (a > 0 && (e = d2h(o_arr + (long long)i * a * b, (long long)a * b))) return e;
+  }
+  return 0;
+}
+
+}  // extern "C"
+
+static int pobtasi_impl(const double* Ld, const double* Ll, const double* La, const double* Lt,
+                        double* Xd, double* Xl, double* Xa, double* Xt, int n, int b, int a,
+                        int has_arrow, int nstart, void* workspace, size_t workspace_bytes,
+                        void* stream, cudaEvent_t ctr_ready, int* persistent) {
   if (Ld == nullptr || Xd == nullptr || n < 1 || b < 1 || a < 0 || nstart > n) return STBTA_EARG;
   if ((n > 1 && (Ll == nullptr || Xl == nullptr)) ||
       (a > 0 && (La == nullptr || Lt == nullptr || Xa == nullptr || Xt == nullptr)))
@@ -611,7 +682,7 @@ int stbta_pobtasi_ex(const double* Ld, const double* Ll, const double* La, const
   const int nta = (a > 0 && full) ? (a + 127) / 128 : 0;
   const int nm = nstart + ((a > 0 && full) ? 1 : 0);
   const int ntm = s.ntb > nta ? s.ntb : nta;
-  if (a > 0 && full && (e = (int)cudaMemsetAsync(ws.Wt, 0, (size_t)a * a * sizeof(double), st))) return e;
+  if (a > 0 && full && (e = zero_async(ws.Wt, (size_t)a * a * sizeof(double), st))) return e;
   inv_diag_tiles_kernel<<<dim3(ntm, nm), SI_NT, smem, st>>>(s);
   count_launch();
   if ((e = (int)cudaGetLastError())) return e;
@@ -621,7 +692,7 @@ int stbta_pobtasi_ex(const double* Ld, const double* Ll, const double* La, const
     if ((e = (int)cudaGetLastError())) return e;
   }
 
-  if (a > 0 && !arrow && (e = (int)cudaMemsetAsync(Xa, 0, (size_t)nstart * a * b * sizeof(double), st)))
+  if (a > 0 && !arrow && (e = zero_async(Xa, (size_t)nstart * a * b * sizeof(double), st)))
     return e;
 
   static const bool use_launches = [] {
@@ -652,7 +723,9 @@ int stbta_pobtasi_ex(const double* Ld, const double* Ll, const double* La, const
     P.ticket = reinterpret_cast<unsigned long long*>(ws.ctr);
     P.abortw = ws.ctr + 2;
     P.ctr = ws.ctr + 4;
-    if ((e = (int)cudaMemsetAsync(ws.ctr, 0, ws.ctr_bytes, st))) return e;
+    if ((e = zero_async(ws.ctr, ws.ctr_bytes, st))) return e;
+    if (ctr_ready && (e = (int)cudaEventRecord(ctr_ready, st))) return e;
+    if (persistent) *persistent = 1;
     static std::atomic<unsigned long long> pmask{0};
     if (attr_pending(pmask)) {
       if ((e = (int)cudaFuncSetAttribute(sinv_persistent_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(SiCfg::SMEM_DOUBLES * sizeof(double))))) return e;
@@ -725,5 +798,3 @@ int stbta_pobtasi_ex(const double* Ld, const double* Ll, const double* La, const
   }
   return 0;
 }
-
-}  // extern "C"

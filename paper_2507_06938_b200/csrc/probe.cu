@@ -93,3 +93,46 @@ int stbta_probe_dmma(int blocks, int iters, double* scratch, void* stream) {
   return (int)cudaGetLastError();
 }
 }
+
+namespace stbta {
+
+__global__ void zero_words_kernel(unsigned long long* p, size_t nwords, unsigned char* tail,
+                                  int ntail) {
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < nwords; i += stride) p[i] = 0ull;
+  if (blockIdx.x == 0 && (int)threadIdx.x < ntail) tail[threadIdx.x] = 0;
+}
+
+int zero_async(void* p, size_t bytes, cudaStream_t st) {
+  if (bytes == 0) return 0;
+  const uintptr_t u = reinterpret_cast<uintptr_t>(p);
+  if (u % 8 != 0) {  // unaligned: byte kernel path through the tail (small buffers only)
+    if (bytes > 256) return (int)cudaMemsetAsync(p, 0, bytes, st);
+    zero_words_kernel<<<1, 256, 0, st>>>(nullptr, 0, reinterpret_cast<unsigned char*>(p), (int)bytes);
+  } else {
+    const size_t nw = bytes / 8;
+    const int ntail = (int)(bytes % 8);
+    int grid = (int)((nw + 255) / 256);
+    if (grid > 1184) grid = 1184;
+    if (grid < 1) grid = 1;
+    zero_words_kernel<<<grid, 256, 0, st>>>(reinterpret_cast<unsigned long long*>(p), nw,
+                                            reinterpret_cast<unsigned char*>(p) + nw * 8, ntail);
+  }
+  count_launch();
+  return (int)cudaGetLastError();
+}
+
+}  // namespace stbta
+
+namespace stbta {
+__global__ void globaltimer_kernel(unsigned long long* out) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  *out = t;
+}
+}  // namespace stbta
+
+extern "C" int stbta_debug_globaltimer(unsigned long long* out, void* stream) {
+  stbta::globaltimer_kernel<<<1, 1, 0, reinterpret_cast<cudaStream_t>(stream)>>>(out);
+  return (int)cudaGetLastError();
+}
