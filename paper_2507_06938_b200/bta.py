@@ -164,11 +164,23 @@ class BTAMatrix:
         n, b = self.n_blocks, self.block_size
         return self.data[: n * b * b].view(n, b, b)
 
+    @diag.setter
+    def diag(self, value):  # `m.diag += x` / `m.diag = x` write through to the buffer
+        view = self.diag
+        if value is not view:
+            view.copy_(value)
+
     @property
     def lower(self):
         n, b = self.n_blocks, self.block_size
         e0 = n * b * b
         return self.data[e0 : e0 + (n - 1) * b * b].view(n - 1, b, b)
+
+    @lower.setter
+    def lower(self, value):  # `m.lower += x` / `m.lower = x` write through to the buffer
+        view = self.lower
+        if value is not view:
+            view.copy_(value)
 
     @property
     def arrow(self):
@@ -176,11 +188,23 @@ class BTAMatrix:
         e1 = (2 * n - 1) * b * b
         return self.data[e1 : e1 + n * a * b].view(n, a, b)
 
+    @arrow.setter
+    def arrow(self, value):  # `m.arrow += x` / `m.arrow = x` write through to the buffer
+        view = self.arrow
+        if value is not view:
+            view.copy_(value)
+
     @property
     def tip(self):
         n, b, a = self.n_blocks, self.block_size, self.arrow_size
         e2 = (2 * n - 1) * b * b + n * a * b
         return self.data[e2:].view(a, a)
+
+    @tip.setter
+    def tip(self, value):  # `m.tip += x` / `m.tip = x` write through to the buffer
+        view = self.tip
+        if value is not view:
+            view.copy_(value)
 
     @property
     def dim(self):

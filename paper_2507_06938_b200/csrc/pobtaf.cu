@@ -108,6 +108,28 @@ STBTA_DEV bool g1_active(const Band& g, int s) {
   return mp >= 2 && band_row(g, s - 1, 1, mb) == s + 1;
 }
 
+// Cross-block updates: tile (R, C) of the NEXT time block (or its arrow rows
+// / the tip), C >= that block's third tile column, is not needed before the
+// current block is fully eliminated, so the updates of CHUNK consecutive
+// panels of the current block are applied as ONE task with K = CHUNK*128
+// (one C-tile load/store and one pipeline fill per CHUNK panels instead of
+// per panel).  The first two tile columns of the next block stay per panel:
+// they feed the next block's first panels.
+constexpr int CHUNK = 4;
+STBTA_DEV bool cross_col(const Band& g, int p, int C) {
+  const int NB = g.n * g.nbt;
+  if (p >= NB) return false;
+  return C >= (p / g.nbt + 1) * g.nbt + 2;
+}
+STBTA_DEV int chunk_first(const Band& g, int p) {
+  const int t = p / g.nbt, j = p - t * g.nbt;
+  return t * g.nbt + (j / CHUNK) * CHUNK;
+}
+STBTA_DEV bool chunk_last(const Band& g, int p) {
+  const int j = p % g.nbt;
+  return (j % CHUNK == CHUNK - 1) || (j == g.nbt - 1);
+}
+
 STBTA_DEV int group_size(const Band& g, int kind, int s) {
   int mb;
   if (s >= g.SP) {  // trailing groups: only the last eliminated panel's bulk (G1, G3)
@@ -120,8 +142,14 @@ STBTA_DEV int group_size(const Band& g, int kind, int s) {
     case 2: return m >= 1 ? NSTRIP : 0;
     case 3: {
       if (s < 1) return 0;
-      const int mp = band_rows(g, s - 1, &mb);
-      const int e = mp >= 2 ? NSTRIP * (mp - 1) + (mp - 1) * (mp - 2) / 2 : 0;
+      const int p = s - 1;
+      const int mp = band_rows(g, p, &mb);
+      const bool last = chunk_last(g, p);
+      int e = 0;
+      for (int j = 1; j < mp; ++j) {
+        if (!last && cross_col(g, p, band_row(g, p, j, mb))) continue;
+        e += NSTRIP + (mp - 1 - j);
+      }
       return e - (g1_active(g, s) ? NSTRIP : 0);
     }
     case 4: return m >= 1 ? NSTRIP * (m - 1) : 0;
@@ -156,7 +184,9 @@ __global__ void __launch_bounds__(1024) dag_setup_kernel(Band g, DagWs ws) {
 
 struct Task {
   int type, s, R, C, q;
+  int s0;  // first panel of a chunked update (== s otherwise)
 };
+
 
 // Group containing ticket t (gstart[lo] <= t < gstart[lo+1]): a 32-ary search
 // by one full warp (3 dependent load rounds instead of ~13 for a binary search).
@@ -179,6 +209,7 @@ STBTA_DEV Task decode(const Band& g, const DagWs& ws, int t, int lo) {
   const int kind = lo % NGRP, s = lo / NGRP;
   int local = t - __ldg(ws.gstart + lo);
   Task k{};
+  k.s0 = -1;
   switch (kind) {
     case 0: k.type = T_TRSM; k.s = s; k.R = s + 1; k.q = local; return k;
     case 1: k.type = T_STRIP; k.s = s - 1; k.R = k.C = s + 1; k.q = local; return k;
@@ -202,12 +233,16 @@ STBTA_DEV Task decode(const Band& g, const DagWs& ws, int t, int lo) {
   int mb;
   const int mp = band_rows(g, p, &mb);
   const bool skip = g1_active(g, s);
+  const bool last = chunk_last(g, p);
   k.s = p;
   for (int j = 1; j < mp; ++j) {
+    const int c = band_row(g, p, j, mb);
+    const bool cross = cross_col(g, p, c);
+    if (cross && !last) continue;
+    k.s0 = cross ? chunk_first(g, p) : p;
     const int ns = (j == 1 && skip) ? 0 : NSTRIP;
     const int cnt = ns + (mp - 1 - j);
     if (local < cnt) {
-      const int c = band_row(g, p, j, mb);
       if (local < ns) { k.type = T_STRIP; k.R = k.C = c; k.q = local; return k; }
       k.type = T_UPD;
       k.R = band_row(g, p, j + 1 + (local - ns), mb);
@@ -346,7 +381,11 @@ __global__ void __launch_bounds__(DAG_NT, 1) pobtaf_dag_kernel(Band g, DagWs ws,
       if (t < total) grp = find_group(ws, t);
       if (tid == 0) {
         s_ticket = t;
-        if (t < total) s_task = decode(g, ws, t, grp);
+        if (t < total) {
+          Task tk2 = decode(g, ws, t, grp);
+          if (tk2.s0 < 0) tk2.s0 = tk2.s;
+          s_task = tk2;
+        }
         s_ok = 1;
       }
     }
@@ -366,15 +405,27 @@ __global__ void __launch_bounds__(DAG_NT, 1) pobtaf_dag_kernel(Band g, DagWs ws,
         if (tid < NSTRIP) { p = counter(g, ws.ctr, s, tid, s); target = need(g, s, s) + 1; }
         else if (tid == NSTRIP) { p = counter(g, ws.ctr, tk.R, tk.q, s); target = need(g, tk.R, s); }
       } else if (tk.type == T_UPD) {
-        if (tid < NSTRIP) { p = counter(g, ws.ctr, tk.R, tid, s); target = need(g, tk.R, s) + 1; }
-        else if (tid < 2 * NSTRIP) { p = counter(g, ws.ctr, tk.C, tid - NSTRIP, s); target = need(g, tk.C, s) + 1; }
-        else if (tid < 3 * NSTRIP) { p = counter(g, ws.ctr, tk.R, tid - 2 * NSTRIP, tk.C); target = n_updates(g, tk.R, tk.C, s); }
+        const int np = s - tk.s0 + 1, nd = NSTRIP * np;  // panels s0..s
+        if (tid < nd) {
+          const int sp = tk.s0 + tid / NSTRIP;
+          p = counter(g, ws.ctr, tk.R, tid % NSTRIP, sp); target = need(g, tk.R, sp) + 1;
+        } else if (tid < 2 * nd) {
+          const int sp = tk.s0 + (tid - nd) / NSTRIP;
+          p = counter(g, ws.ctr, tk.C, (tid - nd) % NSTRIP, sp); target = need(g, tk.C, sp) + 1;
+        } else if (tid < 2 * nd + NSTRIP) {
+          p = counter(g, ws.ctr, tk.R, tid - 2 * nd, tk.C); target = n_updates(g, tk.R, tk.C, tk.s0);
+        }
       } else {  // T_STRIP
-        if (tid <= tk.q) { p = counter(g, ws.ctr, tk.R, tid, s); target = need(g, tk.R, s) + 1; }
-        else if (tid == NSTRIP) { p = counter(g, ws.ctr, tk.R, tk.q, tk.R); target = n_updates(g, tk.R, tk.R, s); }
+        const int np = s - tk.s0 + 1;
+        if (tid < NSTRIP * np) {
+          const int sp = tk.s0 + tid / NSTRIP, q = tid % NSTRIP;
+          if (q <= tk.q) { p = counter(g, ws.ctr, tk.R, q, sp); target = need(g, tk.R, sp) + 1; }
+        } else if (tid == 64) {
+          p = counter(g, ws.ctr, tk.R, tk.q, tk.R); target = n_updates(g, tk.R, tk.R, tk.s0);
+        }
       }
       if (p != nullptr && !spin_geq(p, target, ws.abort_flag)) s_ok = 0;
-      if (tid == 32 && !wait_resident(g, ws, tk.type == T_UPD ? tk.C : tk.type == T_STRIP ? tk.R : s))
+      if (tid == 96 && !wait_resident(g, ws, tk.type == T_UPD ? tk.C : tk.type == T_STRIP ? tk.R : s))
         s_ok = 0;
       __syncthreads();
       if (!s_ok) break;
@@ -443,8 +494,10 @@ __global__ void __launch_bounds__(DAG_NT, 1) pobtaf_dag_kernel(Band g, DagWs ws,
         atomicAdd(counter(g, ws.ctr, tk.R, tk.q, s), 1);
       }
     } else if (tk.type == T_UPD) {
-      const TilePtr rp = tile_ptr(g, tk.R, s);
-      const TilePtr cp = tile_ptr(g, tk.C, s);
+      // panels s0..s of one block: their tile columns are contiguous in storage
+      const int kw = (s - tk.s0) * TT + w;
+      const TilePtr rp = tile_ptr(g, tk.R, tk.s0);
+      const TilePtr cp = tile_ptr(g, tk.C, tk.s0);
       const TilePtr tp = tile_ptr(g, tk.R, tk.C);
       const int er = tile_extent(g, tk.R), ec = tile_extent(g, tk.C);
       double acc[Cfg128::MF][Cfg128::NF][2];
@@ -459,28 +512,29 @@ __global__ void __launch_bounds__(DAG_NT, 1) pobtaf_dag_kernel(Band g, DagWs ws,
         ta = gtimer();
         atomicAdd(ws.prof + 21, ta - t1);
       }
-      tile_mma<Cfg128, true>(acc, A, B, w, 128, smem);
+      tile_mma<Cfg128, true>(acc, A, B, kw, 128, smem);
       if (ws.prof && tid == 0) atomicAdd(ws.prof + 22, gtimer() - ta);
       acc_store<Cfg128>(acc, tp.p, tp.ld, er, ec, 0, 0, 0, 1.0);
       __syncthreads();
       if (tid == 0) {
         __threadfence();
-        for (int q = 0; q < NSTRIP; ++q) atomicAdd(counter(g, ws.ctr, tk.R, q, tk.C), 1);
+        for (int q = 0; q < NSTRIP; ++q) atomicAdd(counter(g, ws.ctr, tk.R, q, tk.C), s - tk.s0 + 1);
       }
     } else {  // T_STRIP
       unsigned long long ta = 0;
       const int ext = tile_extent(g, tk.R);
       const int r0 = tk.q * TS;
       const int rows = min(TS, ext - r0);
+      const int kw = (s - tk.s0) * TT + w;
       if (rows > 0) {
-        const TilePtr xp = tile_ptr(g, tk.R, s);
+        const TilePtr xp = tile_ptr(g, tk.R, tk.s0);
         const TilePtr tp = tile_ptr(g, tk.R, tk.R);
         const int ncol = min(r0 + TS, ext);
         double acc[Cfg32::MF][Cfg32::NF][2];
         acc_load<Cfg32>(acc, tp.p + (long long)r0 * tp.ld, tp.ld, rows, ncol, 1, r0);
         const Opnd A{xp.p + (long long)r0 * xp.ld, xp.ld, rows, xp.vec};
         const Opnd B{xp.p, xp.ld, ncol, xp.vec};
-        tile_mma<Cfg32, true>(acc, A, B, w, ncol, smem);
+        tile_mma<Cfg32, true>(acc, A, B, kw, ncol, smem);
         if (ws.prof && tid == 0) {
           ta = gtimer();
           atomicAdd(ws.prof + 20, ta - t1);
@@ -490,7 +544,7 @@ __global__ void __launch_bounds__(DAG_NT, 1) pobtaf_dag_kernel(Band g, DagWs ws,
       __syncthreads();
       if (tid == 0) {
         __threadfence();
-        atomicAdd(counter(g, ws.ctr, tk.R, tk.q, tk.R), 1);
+        atomicAdd(counter(g, ws.ctr, tk.R, tk.q, tk.R), s - tk.s0 + 1);
       }
     }
     if (ws.prof != nullptr && tid == 0) {

@@ -90,7 +90,7 @@ def test_criterion1_oracle_suite(cuda):
 
 @pytest.mark.parametrize("n,b,a", [(3, 64, 2), (4, 65, 3), (5, 130, 1), (2, 257, 6), (3, 300, 2),
                                    (6, 100, 0), (2, 129, 70), (2, 129, 130), (1, 256, 3),
-                                   (3, 128, 0), (4, 383, 5)])
+                                   (3, 128, 0), (4, 383, 5), (3, 1100, 7), (2, 1025, 0)])
 def test_multileaf_blocks_vs_oracle(cuda, n, b, a):
     """Blocks spanning several 64-leaves and partial leaves, vs the oracle."""
     bta = _bta()
