@@ -115,7 +115,8 @@ STBTA_DEV bool g1_active(const Band& g, int s) {
 // (one C-tile load/store and one pipeline fill per CHUNK panels instead of
 // per panel).  The first two tile columns of the next block stay per panel:
 // they feed the next block's first panels.
-constexpr int CHUNK = 4;
+// CHUNK panels per fused update: 8 for wide blocks (many tile columns), else 4
+STBTA_DEV int chunk_k(const Band& g) { return g.nbt >= 24 ? 8 : 4; }
 STBTA_DEV bool cross_col(const Band& g, int p, int C) {
   const int NB = g.n * g.nbt;
   if (p >= NB) return false;
@@ -123,11 +124,11 @@ STBTA_DEV bool cross_col(const Band& g, int p, int C) {
 }
 STBTA_DEV int chunk_first(const Band& g, int p) {
   const int t = p / g.nbt, j = p - t * g.nbt;
-  return t * g.nbt + (j / CHUNK) * CHUNK;
+  return t * g.nbt + (j / chunk_k(g)) * chunk_k(g);
 }
 STBTA_DEV bool chunk_last(const Band& g, int p) {
   const int j = p % g.nbt;
-  return (j % CHUNK == CHUNK - 1) || (j == g.nbt - 1);
+  return (j % chunk_k(g) == chunk_k(g) - 1) || (j == g.nbt - 1);
 }
 
 STBTA_DEV int group_size(const Band& g, int kind, int s) {
@@ -501,19 +502,12 @@ __global__ void __launch_bounds__(DAG_NT, 1) pobtaf_dag_kernel(Band g, DagWs ws,
       const TilePtr tp = tile_ptr(g, tk.R, tk.C);
       const int er = tile_extent(g, tk.R), ec = tile_extent(g, tk.C);
       double acc[Cfg128::MF][Cfg128::NF][2];
-      acc_load<Cfg128>(acc, tp.p, tp.ld, er, ec, 0, 0);
       const Opnd A{rp.p, rp.ld, er, rp.vec};
       const Opnd B{cp.p, cp.ld, ec, cp.vec};
-      unsigned long long ta = 0;
-      if (ws.prof && tid == 0) {
-        // force the C loads to complete before the stamp (profiling only)
-        double sink = acc[0][0][0];
-        asm volatile("" ::"d"(sink));
-        ta = gtimer();
-        atomicAdd(ws.prof + 21, ta - t1);
-      }
-      tile_mma<Cfg128, true>(acc, A, B, kw, 128, smem);
-      if (ws.prof && tid == 0) atomicAdd(ws.prof + 22, gtimer() - ta);
+      // the C tile loads overlap the first operand slabs' copies
+      tile_mma<Cfg128, true>(acc, A, B, kw, 128, smem, 0,
+                             [&] { acc_load<Cfg128>(acc, tp.p, tp.ld, er, ec, 0, 0); });
+      if (ws.prof && tid == 0) atomicAdd(ws.prof + 22, gtimer() - t1);
       acc_store<Cfg128>(acc, tp.p, tp.ld, er, ec, 0, 0, 0, 1.0);
       __syncthreads();
       if (tid == 0) {
@@ -531,10 +525,11 @@ __global__ void __launch_bounds__(DAG_NT, 1) pobtaf_dag_kernel(Band g, DagWs ws,
         const TilePtr tp = tile_ptr(g, tk.R, tk.R);
         const int ncol = min(r0 + TS, ext);
         double acc[Cfg32::MF][Cfg32::NF][2];
-        acc_load<Cfg32>(acc, tp.p + (long long)r0 * tp.ld, tp.ld, rows, ncol, 1, r0);
         const Opnd A{xp.p + (long long)r0 * xp.ld, xp.ld, rows, xp.vec};
         const Opnd B{xp.p, xp.ld, ncol, xp.vec};
-        tile_mma<Cfg32, true>(acc, A, B, kw, ncol, smem);
+        tile_mma<Cfg32, true>(acc, A, B, kw, ncol, smem, 0, [&] {
+          acc_load<Cfg32>(acc, tp.p + (long long)r0 * tp.ld, tp.ld, rows, ncol, 1, r0);
+        });
         if (ws.prof && tid == 0) {
           ta = gtimer();
           atomicAdd(ws.prof + 20, ta - t1);

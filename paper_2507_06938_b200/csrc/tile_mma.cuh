@@ -102,9 +102,16 @@ STBTA_DEV void load_slab(double* sm, const Opnd& o, int k0, int K) {
 // column is >= n_active skip the arithmetic (triangular strips).  All threads
 // of the CTA must call; smem holds Cfg::SMEM_DOUBLES doubles.  Ends with a
 // __syncthreads so the caller may reuse shared memory.
-template <class Cfg, bool NEG = false, int DBG = 0, bool AKM = false, bool BKM = false>
+struct NoInit {
+  STBTA_DEV void operator()() const {}
+};
+
+// `init` runs after the prologue's slab copies are issued (e.g. the
+// accumulator's C-tile load), so its latency overlaps theirs.
+template <class Cfg, bool NEG = false, int DBG = 0, bool AKM = false, bool BKM = false,
+          class Init = NoInit>
 STBTA_DEV void tile_mma(double (&acc)[Cfg::MF][Cfg::NF][2], const Opnd& A, const Opnd& B, int K,
-                        int n_active, double* smem, int kbeg = 0) {
+                        int n_active, double* smem, int kbeg = 0, const Init& init = Init()) {
   constexpr int MF = Cfg::MF, NF = Cfg::NF, BK = Cfg::BK, ST = Cfg::STAGES, LDS = Cfg::LDS;
   double* As = smem;
   double* Bs = smem + ST * Cfg::A_STAGE;
@@ -126,6 +133,7 @@ STBTA_DEV void tile_mma(double (&acc)[Cfg::MF][Cfg::NF][2], const Opnd& A, const
     if (s < ktiles) load_stage(s, kbeg + s * BK);
     cp_async_commit();
   }
+  init();
   for (int kt = 0; kt < ktiles; ++kt) {
     if (DBG != 1) {  // DBG 1: no waits/barriers (timing experiment only)
       cp_async_wait<ST - 2>();

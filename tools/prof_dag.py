@@ -36,7 +36,7 @@ c = max(p[3], 1); cs = max(p[9], 1)
 print("TRSM: wait->loaded %.2f us, trsm_strip_smem %.2f us, store+signal %.2f us" % (p[18]/c/1e3, p[19]/c/1e3, (p[5]-p[18]-p[19])/c/1e3))
 print("STRIP: load+mma %.2f us, store+signal %.2f us" % (p[20]/cs/1e3, (p[11]-p[20])/cs/1e3))
 cu = max(p[6], 1)
-print("UPDATE: C load %.2f us, tile_mma %.2f us, store+signal %.2f us" % (p[21]/cu/1e3, p[22]/cu/1e3, (p[8]-p[21]-p[22])/cu/1e3))
+print("UPDATE: C load + tile_mma %.2f us, store+signal %.2f us" % (p[22]/cu/1e3, (p[8]-p[22])/cu/1e3))
 import numpy as np
 S = n * ((b + 127) // 128)
 tl = np.array(p[64:64 + 12 * S], dtype=np.int64).reshape(S, 12).astype(np.float64) / 1e3
