@@ -108,27 +108,26 @@ STBTA_DEV bool g1_active(const Band& g, int s) {
   return mp >= 2 && band_row(g, s - 1, 1, mb) == s + 1;
 }
 
-// Cross-block updates: tile (R, C) of the NEXT time block (or its arrow rows
-// / the tip), C >= that block's third tile column, is not needed before the
-// current block is fully eliminated, so the updates of CHUNK consecutive
-// panels of the current block are applied as ONE task with K = CHUNK*128
-// (one C-tile load/store and one pipeline fill per CHUNK panels instead of
-// per panel).  The first two tile columns of the next block stay per panel:
-// they feed the next block's first panels.
-// CHUNK panels per fused update: 8 for wide blocks (many tile columns), else 4
+// Chunked updates: tile (R, C) is first needed when panel C is factored, so
+// the updates of an aligned chunk of CHUNK consecutive panels p of one block
+// whose last panel is at least LOOK panels before C are applied as ONE task
+// with K = CHUNK*128 (one C-tile load/store and one pipeline fill per chunk
+// instead of per panel).  Updates close to the panel front (the next LOOK
+// columns, which the critical chain needs one panel at a time) stay per panel.
+// CHUNK panels per fused update: 8 for wide blocks (many tile columns), else 4.
+constexpr int LOOK = 2;
 STBTA_DEV int chunk_k(const Band& g) { return g.nbt >= 24 ? 8 : 4; }
-STBTA_DEV bool cross_col(const Band& g, int p, int C) {
-  const int NB = g.n * g.nbt;
-  if (p >= NB) return false;
-  return C >= (p / g.nbt + 1) * g.nbt + 2;
-}
 STBTA_DEV int chunk_first(const Band& g, int p) {
   const int t = p / g.nbt, j = p - t * g.nbt;
   return t * g.nbt + (j / chunk_k(g)) * chunk_k(g);
 }
-STBTA_DEV bool chunk_last(const Band& g, int p) {
-  const int j = p % g.nbt;
-  return (j % chunk_k(g) == chunk_k(g) - 1) || (j == g.nbt - 1);
+STBTA_DEV int chunk_end(const Band& g, int p) {
+  return min(chunk_first(g, p) + chunk_k(g) - 1, (p / g.nbt + 1) * g.nbt - 1);
+}
+STBTA_DEV bool chunk_last(const Band& g, int p) { return p == chunk_end(g, p); }
+STBTA_DEV bool cross_col(const Band& g, int p, int C) {
+  if (p >= g.n * g.nbt) return false;
+  return C >= chunk_end(g, p) + 1 + LOOK;
 }
 
 STBTA_DEV int group_size(const Band& g, int kind, int s) {
