@@ -115,7 +115,9 @@ STBTA_DEV bool g1_active(const Band& g, int s) {
 // instead of per panel).  Updates close to the panel front (the next LOOK
 // columns, which the critical chain needs one panel at a time) stay per panel.
 // CHUNK panels per fused update: 8 for wide blocks (many tile columns), else 4.
-constexpr int LOOK = 2;
+// LOOK >= 2 is required: G1 issues panel s-1's update of tile (s+1, s+1) on
+// its own, so that tile must never be part of a chunk.
+STBTA_DEV int look(const Band& g) { return g.nbt >= 24 ? 2 : 3; }
 STBTA_DEV int chunk_k(const Band& g) { return g.nbt >= 24 ? 8 : 4; }
 STBTA_DEV int chunk_first(const Band& g, int p) {
   const int t = p / g.nbt, j = p - t * g.nbt;
@@ -127,7 +129,7 @@ STBTA_DEV int chunk_end(const Band& g, int p) {
 STBTA_DEV bool chunk_last(const Band& g, int p) { return p == chunk_end(g, p); }
 STBTA_DEV bool cross_col(const Band& g, int p, int C) {
   if (p >= g.n * g.nbt) return false;
-  return C >= chunk_end(g, p) + 1 + LOOK;
+  return C >= chunk_end(g, p) + 1 + look(g);
 }
 
 STBTA_DEV int group_size(const Band& g, int kind, int s) {
