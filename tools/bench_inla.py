@@ -56,7 +56,7 @@ def c1():
         "theta_star": res.theta.tolist(), "f_star": res.f,
         "oracle_theta_star": [0.5229479477504098, 0.3853637147715331, -1.085137990668959,
                               1.2627782499940756],
-        "oracle_f_star": -3072.0619154929495,
+        "oracle_f_obj_at_theta_star": -3072.0619154929495,  # minimize reports f_star = -f_obj
     }), flush=True)
 
 
