@@ -60,7 +60,7 @@ def parse_args():
     p.add_argument("--config", default="c2", choices=["c2", "c5"],
                    help="c2: BTA microbench (default); c5: distributed POBTAF weak scaling, "
                         "96 time blocks per GPU, one partition per rank over NCCL")
-    p.add_argument("--lb", type=float, default=1.0, help="C5 load-balance factor")
+    p.add_argument("--lb", type=float, default=1.6, help="C5 load-balance factor (plan_partitions lb; 1.6 measured best at 2 and 4 GPUs)")
     p.add_argument("--no-inla", action="store_true",
                    help="skip the C3 f_obj measurement (north-star model, rank 0 at N=1)")
     return p.parse_args()
