@@ -21,6 +21,13 @@ struct MemOps {
 // Resolved once per process; ok == false when the driver lacks them.
 const MemOps& memops();
 
+// cuTensorMapEncodeTiled (driver), nullptr when unavailable.
+using TensorMapEncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                       const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                       const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                       CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+TensorMapEncodeFn tensor_map_encode();
+
 inline int memops_write(cudaStream_t st, const void* addr, unsigned v) {
   const MemOps& m = memops();
   if (!m.ok) return (int)cudaErrorNotSupported;

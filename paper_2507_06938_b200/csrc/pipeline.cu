@@ -35,6 +35,19 @@ const MemOps& memops() {
   return m;
 }
 
+TensorMapEncodeFn tensor_map_encode() {
+  static TensorMapEncodeFn f = [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult st = cudaDriverEntryPointSymbolNotFound;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &st) != cudaSuccess ||
+        st != cudaDriverEntryPointSuccess)
+      fn = nullptr;
+    cudaGetLastError();
+    return reinterpret_cast<TensorMapEncodeFn>(fn);
+  }();
+  return f;
+}
+
 }  // namespace stbta
 
 using namespace stbta;

@@ -24,6 +24,7 @@
 // pivot sets info (1 + time block, n+1 for the tip) and an abort word that
 // drains the kernel.  Log-det partials per panel are summed in a fixed order.
 #include <cub/block/block_scan.cuh>
+#include <cstdlib>
 #include <cstring>
 
 #include "../../include/stbta.h"
@@ -31,6 +32,8 @@
 #include "potrf_tile.cuh"
 #include "stbta_internal.cuh"
 #include "tile_mma.cuh"
+#include "tma_mma.cuh"
+#include "memops.cuh"
 
 namespace stbta {
 
@@ -40,7 +43,7 @@ using Cfg32 = MmaCfg<32, 128, 32, 16, DAG_NT>;
 constexpr int TRSM_SMEM_DOUBLES = 32 * 132 + 128 * 132 + 4 * 32 * PT_WLD;
 constexpr int cmax(int x, int y) { return x > y ? x : y; }
 constexpr int DAG_SMEM_DOUBLES =
-    cmax(cmax(PT_SMEM_DOUBLES, TRSM_SMEM_DOUBLES), Cfg128::SMEM_DOUBLES);
+    cmax(cmax(cmax(PT_SMEM_DOUBLES, TRSM_SMEM_DOUBLES), Cfg128::SMEM_DOUBLES), TMA_SMEM_DOUBLES);
 constexpr int W_SLOT = 4 * 32 * 32;  // per panel: the four W_kk^T blocks
 constexpr size_t DAG_SMEM_BYTES = DAG_SMEM_DOUBLES * sizeof(double);
 
@@ -259,6 +262,32 @@ STBTA_DEV Task decode(const Band& g, const DagWs& ws, int t, int lo) {
 
 STBTA_DEV int need(const Band& g, int R, int C) { return n_updates(g, R, C, C); }
 
+// Tensor maps of the diag / lower / arrow regions (rows x b, row stride ldb),
+// 16 x 128 boxes, 128-byte swizzle; ok[i] == 0 when a region is not eligible.
+struct TmaMaps {
+  CUtensorMap m[3];
+  int ok[3];
+};
+
+STBTA_DEV TmaOpnd tile_tma(const Band& g, const TmaMaps& tm, int R, int C) {
+  TmaOpnd o{nullptr, 0, 0};
+  const int NB = g.n * g.nbt;
+  if (C >= NB) return o;  // tip: no map
+  const int tc = C / g.nbt, jc = C % g.nbt;
+  o.col = jc * TT;
+  int r;
+  if (R >= NB) {
+    r = 2;
+    o.row = tc * g.a + (R - NB) * TT;
+  } else {
+    const int tr = R / g.nbt, jr = R % g.nbt;
+    r = (tr == tc) ? 0 : 1;
+    o.row = tc * g.b + jr * TT;
+  }
+  if (tm.ok[r]) o.map = &tm.m[r];
+  return o;
+}
+
 // The panel worker: POTRF(s) for s = 0..S-1 in order, on one dedicated CTA
 // (its instruction cache stays warm with the factorization code, and the
 // panel chain never queues behind bulk updates).  Returns false on abort.
@@ -359,7 +388,8 @@ STBTA_DEV bool potrf_worker(const Band& g, const DagWs& ws, int* info, double* s
   return true;
 }
 
-__global__ void __launch_bounds__(DAG_NT, 1) pobtaf_dag_kernel(Band g, DagWs ws, int* info) {
+__global__ void __launch_bounds__(DAG_NT, 1) pobtaf_dag_kernel(Band g, DagWs ws, int* info,
+                                                              const __grid_constant__ TmaMaps tm) {
   extern __shared__ __align__(16) double smem[];
   __shared__ int s_ticket, s_ok;
   __shared__ Task s_task;
@@ -373,6 +403,9 @@ __global__ void __launch_bounds__(DAG_NT, 1) pobtaf_dag_kernel(Band g, DagWs ws,
     potrf_worker(g, ws, info, smem);
     return;
   }
+  __shared__ unsigned long long s_tbars[TMA_ST];
+  tma_bars_init(s_tbars);
+  unsigned tphase = 0;
 
   for (;;) {
     if (tid < 32) {
@@ -506,8 +539,12 @@ __global__ void __launch_bounds__(DAG_NT, 1) pobtaf_dag_kernel(Band g, DagWs ws,
       const Opnd A{rp.p, rp.ld, er, rp.vec};
       const Opnd B{cp.p, cp.ld, ec, cp.vec};
       // the C tile loads overlap the first operand slabs' copies
-      tile_mma<Cfg128, true>(acc, A, B, kw, 128, smem, 0,
-                             [&] { acc_load<Cfg128>(acc, tp.p, tp.ld, er, ec, 0, 0); });
+      auto cload = [&] { acc_load<Cfg128>(acc, tp.p, tp.ld, er, ec, 0, 0); };
+      const TmaOpnd ta = tile_tma(g, tm, tk.R, tk.s0), tb = tile_tma(g, tm, tk.C, tk.s0);
+      if (ta.map != nullptr && tb.map != nullptr && kw % 32 == 0)
+        tile_mma_tma<Cfg128, true>(acc, ta, tb, kw, smem, s_tbars, tphase, cload);
+      else
+        tile_mma<Cfg128, true>(acc, A, B, kw, 128, smem, 0, cload);
       if (ws.prof && tid == 0) atomicAdd(ws.prof + 22, gtimer() - t1);
       acc_store<Cfg128>(acc, tp.p, tp.ld, er, ec, 0, 0, 0, 1.0);
       __syncthreads();
@@ -630,6 +667,35 @@ static size_t dag_ws(const Band& g, char* base, DagWs* o, size_t* zero_bytes) {
   return gs + cz + sl + wb;
 }
 
+// One 2D tensor map per storage region (diag, lower, arrow): width b columns,
+// height = the region's rows, row stride ldb doubles.  Disabled (ok = 0) when
+// the driver entry point is missing, rows are not 16-byte aligned (odd ldb),
+// or STBTA_NO_TMA=1 is set.
+static void make_tma_maps(const Band& g, TmaMaps* tm) {
+  memset(tm, 0, sizeof(*tm));
+  static const bool off = [] {
+    const char* v = getenv("STBTA_NO_TMA");
+    return v && v[0] == '1';
+  }();
+  TensorMapEncodeFn enc = tensor_map_encode();
+  if (off || enc == nullptr || !g.vec_b) return;
+  const double* base[3] = {g.dg, g.lw, g.ar};
+  const long long rows[3] = {(long long)g.n * g.b, (long long)(g.n - 1) * g.b,
+                             g.use_arrow ? (long long)g.n * g.a : 0};
+  for (int r = 0; r < 3; ++r) {
+    if (base[r] == nullptr || rows[r] <= 0 || ((uintptr_t)base[r] % 16) != 0) continue;
+    const cuuint64_t dims[2] = {(cuuint64_t)g.b, (cuuint64_t)rows[r]};
+    const cuuint64_t strides[1] = {(cuuint64_t)g.ldb * sizeof(double)};
+    const cuuint32_t box[2] = {16, 128};
+    const cuuint32_t es[2] = {1, 1};
+    const CUresult e = enc(&tm->m[r], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base[r]),
+                           dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    tm->ok[r] = (e == CUDA_SUCCESS) ? 1 : 0;
+  }
+}
+
 static int sm_count() {
   int dev = 0, v = 148;
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
@@ -729,7 +795,9 @@ static int pobtaf_impl(double* diag, double* lower, double* arrow, double* tip, 
   dag_setup_kernel<<<1, 1024, 0, st>>>(g, ws);
   count_launch();
   if ((e = (int)cudaGetLastError())) return e;
-  pobtaf_dag_kernel<<<sm_count(), DAG_NT, DAG_SMEM_BYTES, st>>>(g, ws, info);
+  TmaMaps tm;
+  make_tma_maps(g, &tm);
+  pobtaf_dag_kernel<<<sm_count(), DAG_NT, DAG_SMEM_BYTES, st>>>(g, ws, info, tm);
   count_launch();
   if ((e = (int)cudaGetLastError())) return e;
   if (logdet_out != nullptr) {

@@ -1,0 +1,120 @@
+// TMA-staged variant of tile_mma for 128 x 128 tiles whose operands are both
+// K-contiguous row sets of a region described by a CUtensorMap (POBTAF UPDATE):
+//
+//   acc(128 x 128) (+)= A(128 x K) * B(128 x K)^T,   K % 32 == 0
+//
+// Thread 0 streams each 32-wide K slab of A and B with four
+// cp.async.bulk.tensor.2d copies (16 x 128 boxes, 128-byte swizzle) onto a
+// per-stage mbarrier (complete_tx), so the global->shared traffic bypasses the
+// LSU pipe that feeds the DMMA fragment loads; the 128-byte swizzle makes the
+// 8x4 fragment reads conflict-free without padding.  Rows beyond the tile
+// (partial tiles) come in as whatever lies there and only feed output rows /
+// columns the caller does not store; columns >= the tensor width read as zero.
+#pragma once
+
+#include <cuda.h>
+
+#include "tile_mma.cuh"
+
+namespace stbta {
+
+struct TmaOpnd {
+  const CUtensorMap* map;  // nullptr: not TMA-eligible
+  int row, col;            // tile origin in the tensor (row, first K column)
+};
+
+constexpr int TMA_ST = 3;                      // pipeline stages
+constexpr int TMA_HALF = 128 * 16;             // doubles per 16-column box
+constexpr int TMA_OPND = 2 * TMA_HALF;         // one operand, one 32-wide slab
+constexpr int TMA_STAGE = 2 * TMA_OPND;        // A + B
+constexpr unsigned TMA_STAGE_BYTES = TMA_STAGE * 8;
+constexpr int TMA_SMEM_DOUBLES = TMA_ST * TMA_STAGE + 128;  // + 1 KB alignment slack
+
+STBTA_DEV void tma_load_2d(double* dst, const CUtensorMap* map, int col, int row,
+                           unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];\n" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<unsigned long long>(map)), "r"(col), "r"(row), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// 1 KB-aligned staging base inside `smem` (128-byte swizzle atoms are 1 KB).
+STBTA_DEV double* tma_stage_base(double* smem) {
+  const unsigned a = smem_u32(smem);
+  return smem + (((a + 1023u) & ~1023u) - a) / 8;
+}
+
+// Call once per CTA before the first tile_mma_tma (thread 0 initialises).
+STBTA_DEV void tma_bars_init(unsigned long long* bars) {
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < TMA_ST; ++s) mbar_init(bars + s, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+}
+
+// `phase`: per-stage parity bits, identical in all threads, carried across calls.
+template <class Cfg, bool NEG = false, class Init = NoInit>
+STBTA_DEV void tile_mma_tma(double (&acc)[Cfg::MF][Cfg::NF][2], const TmaOpnd& A,
+                            const TmaOpnd& B, int K, double* smem, unsigned long long* bars,
+                            unsigned& phase, const Init& init = Init()) {
+  static_assert(Cfg::BM == 128 && Cfg::BN == 128, "TMA path is laid out for 128 x 128 tiles");
+  constexpr int MF = Cfg::MF, NF = Cfg::NF;
+  double* base = tma_stage_base(smem);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int gq = lane >> 2, tq = lane & 3;
+  const int wm0 = (warp % Cfg::WARPS_M) * Cfg::WM;
+  const int wn0 = (warp / Cfg::WARPS_M) * Cfg::WN;
+  const int nk = K / 32;
+  auto issue = [&](int kt) {  // thread 0
+    double* st = base + (kt % TMA_ST) * TMA_STAGE;
+    unsigned long long* bar = bars + kt % TMA_ST;
+    mbar_expect_tx(bar, TMA_STAGE_BYTES);
+    const int k0 = kt * 32;
+    tma_load_2d(st, A.map, A.col + k0, A.row, bar);
+    tma_load_2d(st + TMA_HALF, A.map, A.col + k0 + 16, A.row, bar);
+    tma_load_2d(st + TMA_OPND, B.map, B.col + k0, B.row, bar);
+    tma_load_2d(st + TMA_OPND + TMA_HALF, B.map, B.col + k0 + 16, B.row, bar);
+  };
+  if (tid == 0) {
+    // earlier generic-proxy shared-memory writes (other task kinds) before async writes
+    asm volatile("fence.proxy.async;\n" ::: "memory");
+#pragma unroll
+    for (int s = 0; s < TMA_ST - 1; ++s)
+      if (s < nk) issue(s);
+  }
+  init();
+  // per-lane swizzled offsets: element (r, k) of a box at r*16 + (((k>>1) ^ (r&7)) << 1) + (k&1)
+  int swz[4];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) swz[c] = ((((c * 2) + (tq >> 1)) ^ gq) << 1) + (tq & 1);
+  for (int kt = 0; kt < nk; ++kt) {
+    const int s = kt % TMA_ST;
+    mbar_wait(bars + s, (phase >> s) & 1u);
+    phase ^= 1u << s;
+    __syncthreads();  // every warp is done with the stage the next copy overwrites
+    if (tid == 0 && kt + TMA_ST - 1 < nk) issue(kt + TMA_ST - 1);
+    const double* as = base + s * TMA_STAGE;
+    const double* bs = as + TMA_OPND;
+#pragma unroll
+    for (int ks = 0; ks < 8; ++ks) {
+      const int h = (ks >> 2) * TMA_HALF, o = swz[ks & 3];
+      double af[MF], bf[NF];
+#pragma unroll
+      for (int i = 0; i < MF; ++i) af[i] = as[h + (wm0 + i * 8 + gq) * 16 + o];
+#pragma unroll
+      for (int j = 0; j < NF; ++j) {
+        const double bv = bs[h + (wn0 + j * 8 + gq) * 16 + o];
+        bf[j] = NEG ? -bv : bv;
+      }
+#pragma unroll
+      for (int i = 0; i < MF; ++i)
+#pragma unroll
+        for (int j = 0; j < NF; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
+  }
+  __syncthreads();
+}
+
+}  // namespace stbta
