@@ -18,12 +18,14 @@
 //     triangular structure of W used to skip the zero K-range and X_ii formed
 //     on its lower tiles and mirrored.
 #include <cstdlib>
+#include <cstring>
 
 #include "../../include/stbta.h"
 #include "band.cuh"
 #include "potrf_tile.cuh"
 #include "stbta_internal.cuh"
 #include "tile_mma.cuh"
+#include "tma_mma.cuh"
 #include "memops.cuh"
 
 namespace stbta {
@@ -43,6 +45,20 @@ struct Prod {
   long long ldb;
   int K, akm, bkm, ktri, arows_all;
   double sgn;
+  int amap, bmap;  // tensor-map index of the operand region (-1: none)
+  int ablk, bblk;  // block of the region holding the operand
+};
+
+// Tensor maps of the recursion's operand regions (persistent kernel only).
+enum { SM_XD = 0, SM_LL, SM_W, SM_T1, SM_T3, SM_XL, SM_NMAP };
+struct SiMaps {
+  CUtensorMap m[SM_NMAP];
+  int ok[SM_NMAP];
+};
+struct TmaCtx {
+  const SiMaps* maps;
+  unsigned long long* bars;
+  unsigned* phase;
 };
 
 struct TileJob {
@@ -61,7 +77,20 @@ struct TileJob {
 
 template <class Cfg, bool AKM, bool BKM>
 STBTA_DEV void run_prod(double (&acc)[Cfg::MF][Cfg::NF][2], const Prod& p, int tr, int tc,
-                        int mrows, int ncols, double* smem) {
+                        int mrows, int ncols, double* smem, const TmaCtx* tc_) {
+  if constexpr (Cfg::BM == 128) {
+    if (tc_ != nullptr && p.amap >= 0 && p.bmap >= 0 && tc_->maps->ok[p.amap] &&
+        tc_->maps->ok[p.bmap]) {
+      const int kb = p.ktri ? tc * 128 : 0;
+      if (kb >= p.K) return;
+      if ((p.K - kb) % 32 == 0) {
+        const TmaOpnd3 ta{&tc_->maps->m[p.amap], tr * 128, p.ablk};
+        const TmaOpnd3 tb{&tc_->maps->m[p.bmap], tc * 128, p.bblk};
+        tile_mma_tma3<Cfg, AKM, BKM>(acc, ta, tb, kb, p.K, smem, tc_->bars, *tc_->phase);
+        return;
+      }
+    }
+  }
   Opnd a{AKM ? p.A + tr * Cfg::BM : p.A + (long long)tr * Cfg::BM * p.lda, p.lda, mrows, 0};
   Opnd b{BKM ? p.B + tc * 128 : p.B + (long long)tc * 128 * p.ldb, p.ldb, ncols, 0};
   a.vec = ((uintptr_t)a.p % 16 == 0) && (a.ld % 2 == 0);
@@ -81,7 +110,8 @@ STBTA_DEV void acc_neg(double (&acc)[Cfg::MF][Cfg::NF][2]) {
 
 // One output tile (BM x 128) of a job: init, signed products, store (+ mirror).
 template <class Cfg>
-STBTA_DEV void tile_job_body(const TileJob& j, int tr, int tc, double* smem) {
+STBTA_DEV void tile_job_body(const TileJob& j, int tr, int tc, double* smem,
+                             const TmaCtx* tx = nullptr) {
   const int mrows = min(Cfg::BM, j.M - tr * Cfg::BM), ncols = min(128, j.N - tc * 128);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, gq = lane >> 2, tq = lane & 3;
   const int wm0 = (warp % Cfg::WARPS_M) * Cfg::WM, wn0 = (warp / Cfg::WARPS_M) * Cfg::WN;
@@ -107,10 +137,10 @@ STBTA_DEV void tile_job_body(const TileJob& j, int tr, int tc, double* smem) {
   for (int q = 0; q < j.nprod; ++q) {
     const Prod& p = j.p[q];
     if (p.sgn < 0) acc_neg<Cfg>(acc);
-    if (p.akm && p.bkm) run_prod<Cfg, true, true>(acc, p, tr, tc, mrows, ncols, smem);
-    else if (p.akm) run_prod<Cfg, true, false>(acc, p, tr, tc, mrows, ncols, smem);
-    else if (p.bkm) run_prod<Cfg, false, true>(acc, p, tr, tc, mrows, ncols, smem);
-    else run_prod<Cfg, false, false>(acc, p, tr, tc, mrows, ncols, smem);
+    if (p.akm && p.bkm) run_prod<Cfg, true, true>(acc, p, tr, tc, mrows, ncols, smem, tx);
+    else if (p.akm) run_prod<Cfg, true, false>(acc, p, tr, tc, mrows, ncols, smem, tx);
+    else if (p.bkm) run_prod<Cfg, false, true>(acc, p, tr, tc, mrows, ncols, smem, tx);
+    else run_prod<Cfg, false, false>(acc, p, tr, tc, mrows, ncols, smem, tx);
     if (p.sgn < 0) acc_neg<Cfg>(acc);
   }
   acc_store<Cfg>(acc, j.C + (long long)r0 * j.ldc + c0, j.ldc, mrows, ncols, 0, 0, 0, j.alpha);
@@ -320,10 +350,11 @@ STBTA_DEV void make_job(const SiParams& P, int kind, int i, TileJob& j) {
   j = TileJob{};
   j.alpha = 1.0;
   auto pr = [](const double* A, long long lda, int akm, const double* B, long long ldb, int bkm,
-               int K, double sgn, int ktri) {
+               int K, double sgn, int ktri, int am = -1, int ab = 0, int bm = -1, int bblk = 0) {
     Prod p{};
     p.A = A; p.lda = lda; p.akm = akm; p.B = B; p.ldb = ldb; p.bkm = bkm;
     p.K = K; p.sgn = sgn; p.ktri = ktri;
+    p.amap = am; p.ablk = ab; p.bmap = bm; p.bblk = bblk;
     return p;
   };
   switch (kind) {
@@ -334,7 +365,7 @@ STBTA_DEV void make_job(const SiParams& P, int kind, int i, TileJob& j) {
       break;
     case K_T1:
       j.C = P.T1[par]; j.ldc = b; j.M = b; j.N = b;
-      j.p[j.nprod++] = pr(P.Xd + (i + 1) * bb, b, 0, sub, b, 1, b, 1.0, 0);
+      j.p[j.nprod++] = pr(P.Xd + (i + 1) * bb, b, 0, sub, b, 1, b, 1.0, 0, SM_XD, i + 1, SM_LL, i);
       if (arr) j.p[j.nprod++] = pr(P.Xa + (long long)(i + 1) * a * b, b, 1, arr, b, 1, a, 1.0, 0);
       break;
     case K_XA:
@@ -343,18 +374,18 @@ STBTA_DEV void make_job(const SiParams& P, int kind, int i, TileJob& j) {
       break;
     case K_XL:
       j.C = P.Xl + i * bb; j.ldc = b; j.M = b; j.N = b; j.alpha = -1.0;
-      j.p[j.nprod++] = pr(P.T1[par], b, 0, W, b, 1, b, 1.0, 1);
+      j.p[j.nprod++] = pr(P.T1[par], b, 0, W, b, 1, b, 1.0, 1, SM_T1, par, SM_W, i);
       break;
     case K_T3:
       j.C = P.T3[par]; j.ldc = b; j.M = b; j.N = b;
       j.init = 2; j.ci = W; j.ldci = b;
-      if (sub) j.p[j.nprod++] = pr(P.Xl + i * bb, b, 1, sub, b, 1, b, -1.0, 0);
+      if (sub) j.p[j.nprod++] = pr(P.Xl + i * bb, b, 1, sub, b, 1, b, -1.0, 0, SM_XL, i, SM_LL, i);
       if (arr) j.p[j.nprod++] = pr(P.Xa + (long long)i * a * b, b, 1, arr, b, 1, a, -1.0, 0);
       break;
     default:  // K_XII
       j.C = P.Xd + i * bb; j.ldc = b; j.M = b; j.N = b;
       j.lower = 1; j.mirror = 1;
-      j.p[j.nprod++] = pr(P.T3[par], b, 0, W, b, 1, b, 1.0, 1);
+      j.p[j.nprod++] = pr(P.T3[par], b, 0, W, b, 1, b, 1.0, 1, SM_T3, par, SM_W, i);
       break;
   }
 }
@@ -406,8 +437,16 @@ STBTA_DEV void wait_all(const SiParams& P, int kind, int i, int tr) {
   }
 }
 
-__global__ void __launch_bounds__(SI_NT, 1) sinv_persistent_kernel(SiParams P) {
+constexpr int SIP_SMEM_DOUBLES =
+    SiCfg::SMEM_DOUBLES > TMA_SMEM_DOUBLES ? SiCfg::SMEM_DOUBLES : TMA_SMEM_DOUBLES;
+
+__global__ void __launch_bounds__(SI_NT, 1) sinv_persistent_kernel(SiParams P,
+                                                                   const __grid_constant__ SiMaps maps) {
   extern __shared__ __align__(16) double smem[];
+  __shared__ unsigned long long s_tbars[TMA_ST];
+  tma_bars_init(s_tbars);
+  unsigned tphase = 0;
+  const TmaCtx tx{&maps, s_tbars, &tphase};
   __shared__ TileJob s_job;
   __shared__ int s_info[4];  // kind, i, tr, tc (+ small flag in kind's high bit)
   for (;;) {
@@ -460,7 +499,7 @@ __global__ void __launch_bounds__(SI_NT, 1) sinv_persistent_kernel(SiParams P) {
     const int kinfo = s_info[0], i = s_info[1], tr = s_info[2], tc = s_info[3];
     if (kinfo == -2) return;
     if (kinfo & 0x100) tile_job_body<SiCfg32>(s_job, tr, tc, smem);
-    else tile_job_body<SiCfg>(s_job, tr, tc, smem);
+    else tile_job_body<SiCfg>(s_job, tr, tc, smem, &tx);
     __syncthreads();
     if (threadIdx.x == 0) {
       int* c = ctr_slot(P, i, kinfo & 0xff);
@@ -512,6 +551,49 @@ static size_t pobtasi_ws(int n, int b, int a, char* base, PobtasiWs* o) {
     o->ctr_bytes = ctr;
   }
   return wall + wt + 4 * bb + 2 * ta + tmp + ctr;
+}
+
+// 3D tensor maps {b columns, b rows, blocks} (row stride b doubles) of the
+// recursion's b x b operand regions: row-major operands with 16 x 128 boxes,
+// k-major ones with 16 x 32 boxes (tma_mma.cuh).  None when b is odd (rows not
+// 16-byte aligned), the driver entry point is missing or STBTA_NO_TMA=1.
+static void make_si_maps(const SiParams& P, const PobtasiWs& ws, SiMaps* mp) {
+  memset(mp, 0, sizeof(*mp));
+  static const bool off = [] {
+    const char* v = getenv("STBTA_NO_TMA");
+    return v && v[0] == '1';
+  }();
+  TensorMapEncodeFn enc = tensor_map_encode();
+  const int b = P.b;
+  if (off || enc == nullptr || (b % 2) != 0) return;
+  const unsigned long long bbytes = (unsigned long long)b * b * sizeof(double);
+  struct R {
+    const double* base;
+    int blocks;
+    unsigned long long bstride;
+    int kmajor;
+  } reg[SM_NMAP] = {
+      {P.Xd, P.n, bbytes, 0},
+      {P.Ll, P.n - 1, bbytes, 1},
+      {P.W, P.nstart, bbytes, 1},
+      {P.T1[0], 2, (unsigned long long)((const char*)P.T1[1] - (const char*)P.T1[0]), 0},
+      {P.T3[0], 2, (unsigned long long)((const char*)P.T3[1] - (const char*)P.T3[0]), 0},
+      {P.Xl, P.n - 1, bbytes, 1},
+  };
+  for (int r = 0; r < SM_NMAP; ++r) {
+    if (reg[r].base == nullptr || reg[r].blocks < 1 || ((uintptr_t)reg[r].base % 16) != 0 ||
+        (reg[r].bstride % 16) != 0)
+      continue;
+    const cuuint64_t dims[3] = {(cuuint64_t)b, (cuuint64_t)b, (cuuint64_t)reg[r].blocks};
+    const cuuint64_t strides[2] = {(cuuint64_t)b * sizeof(double), (cuuint64_t)reg[r].bstride};
+    const cuuint32_t box[3] = {16, reg[r].kmajor ? 32u : 128u, 1};
+    const cuuint32_t es[3] = {1, 1, 1};
+    const CUresult e = enc(&mp->m[r], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3,
+                           const_cast<double*>(reg[r].base), dims, strides, box, es,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    mp->ok[r] = (e == CUDA_SUCCESS) ? 1 : 0;
+  }
 }
 
 static int sm_count() {
@@ -727,18 +809,20 @@ static int pobtasi_impl(const double* Ld, const double* Ll, const double* La, co
     if (ctr_ready && (e = (int)cudaEventRecord(ctr_ready, st))) return e;
     if (persistent) *persistent = 1;
     static std::atomic<unsigned long long> pmask{0};
+    const size_t psmem = SIP_SMEM_DOUBLES * sizeof(double);
     if (attr_pending(pmask)) {
-      if ((e = (int)cudaFuncSetAttribute(sinv_persistent_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(SiCfg::SMEM_DOUBLES * sizeof(double))))) return e;
+      if ((e = (int)cudaFuncSetAttribute(sinv_persistent_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem))) return e;
       attr_mark(pmask);
     }
+    SiMaps maps;
+    make_si_maps(P, ws, &maps);
     int occ = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sinv_persistent_kernel, SI_NT,
-                                                  SiCfg::SMEM_DOUBLES * sizeof(double));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sinv_persistent_kernel, SI_NT, psmem);
     if (occ < 1) return STBTA_EARG;
     long long grid = (long long)sm_count() * occ;
     if (grid > P.total) grid = P.total;
     if (grid < 1) return 0;
-    sinv_persistent_kernel<<<(int)grid, SI_NT, SiCfg::SMEM_DOUBLES * sizeof(double), st>>>(P);
+    sinv_persistent_kernel<<<(int)grid, SI_NT, psmem, st>>>(P, maps);
     count_launch();
     return (int)cudaGetLastError();
   }

@@ -118,3 +118,103 @@ STBTA_DEV void tile_mma_tma(double (&acc)[Cfg::MF][Cfg::NF][2], const TmaOpnd& A
 }
 
 }  // namespace stbta
+
+// ---------------------------------------------------------------------------
+// General orientation (POBTASI tile jobs): each operand is either row-major
+// (element (r, k) at p[r*ld + k]: tensor {K, rows, blocks}, 16 x 128 boxes) or
+// k-major (element (r, k) at p[k*ld + r]: tensor {rows, K, blocks}, 16 x 32
+// boxes), 128-byte swizzle in both cases.  To keep the fragment reads
+// conflict-free for BOTH layouts, k-step ks reads physical slab columns
+// kp = KB[ks] + {0, 1, 4, 5}[tq] (a permutation of 0..31, identical for A and
+// B, so the product is unchanged): kp's bit 0 alternates across the lane
+// quads (row-major: the two 8-byte halves of a chunk) and bit 2 alternates
+// (k-major: the swizzle XOR moves between chunk groups).
+namespace stbta {
+
+struct TmaOpnd3 {
+  const CUtensorMap* map;  // nullptr: not TMA-eligible
+  int r0;                  // first row (m or n) of the tile
+  int blk;                 // block index (3rd tensor dimension)
+};
+
+STBTA_DEV void tma_load_3d(double* dst, const CUtensorMap* map, int c0, int c1, int c2,
+                           unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<unsigned long long>(map)), "r"(c0), "r"(c1), "r"(c2),
+      "r"(smem_u32(bar))
+      : "memory");
+}
+
+template <bool KM>
+STBTA_DEV void tma_issue_opnd(double* dst, const TmaOpnd3& o, int k0, unsigned long long* bar) {
+  if (!KM) {
+    tma_load_3d(dst, o.map, k0, o.r0, o.blk, bar);
+    tma_load_3d(dst + TMA_HALF, o.map, k0 + 16, o.r0, o.blk, bar);
+  } else {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) tma_load_3d(dst + i * 512, o.map, o.r0 + 16 * i, k0, o.blk, bar);
+  }
+}
+
+// offset of element (r, kp) of one operand's slab; r = rb + gq with rb % 8 == 0
+template <bool KM>
+STBTA_DEV int tma_off(int r, int kp) {
+  if (!KM) return (kp >> 4) * TMA_HALF + r * 16 + ((((kp & 15) >> 1) ^ (r & 7)) << 1) + (kp & 1);
+  return (r >> 4) * 512 + kp * 16 + ((((r & 15) >> 1) ^ (kp & 7)) << 1) + (r & 1);
+}
+
+// acc += A * B^T over k in [kbeg, K), (K - kbeg) % 32 == 0.
+template <class Cfg, bool AKM, bool BKM>
+STBTA_DEV void tile_mma_tma3(double (&acc)[Cfg::MF][Cfg::NF][2], const TmaOpnd3& A,
+                             const TmaOpnd3& B, int kbeg, int K, double* smem,
+                             unsigned long long* bars, unsigned& phase) {
+  static_assert(Cfg::BM == 128 && Cfg::BN == 128, "TMA path is laid out for 128 x 128 tiles");
+  constexpr int MF = Cfg::MF, NF = Cfg::NF;
+  double* base = tma_stage_base(smem);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int gq = lane >> 2, tq = lane & 3;
+  const int wm0 = (warp % Cfg::WARPS_M) * Cfg::WM;
+  const int wn0 = (warp / Cfg::WARPS_M) * Cfg::WN;
+  const int nk = (K - kbeg) / 32;
+  auto issue = [&](int kt) {  // thread 0
+    double* st = base + (kt % TMA_ST) * TMA_STAGE;
+    unsigned long long* bar = bars + kt % TMA_ST;
+    mbar_expect_tx(bar, TMA_STAGE_BYTES);
+    tma_issue_opnd<AKM>(st, A, kbeg + kt * 32, bar);
+    tma_issue_opnd<BKM>(st + TMA_OPND, B, kbeg + kt * 32, bar);
+  };
+  if (tid == 0) {
+    asm volatile("fence.proxy.async;\n" ::: "memory");
+#pragma unroll
+    for (int s = 0; s < TMA_ST - 1; ++s)
+      if (s < nk) issue(s);
+  }
+  const int o4 = (tq & 1) + 4 * (tq >> 1);  // {0, 1, 4, 5}
+  for (int kt = 0; kt < nk; ++kt) {
+    const int s = kt % TMA_ST;
+    mbar_wait(bars + s, (phase >> s) & 1u);
+    phase ^= 1u << s;
+    __syncthreads();
+    if (tid == 0 && kt + TMA_ST - 1 < nk) issue(kt + TMA_ST - 1);
+    const double* as = base + s * TMA_STAGE;
+    const double* bs = as + TMA_OPND;
+#pragma unroll
+    for (int ks = 0; ks < 8; ++ks) {
+      const int kp = (ks >> 1) * 8 + (ks & 1) * 2 + o4;  // KB = {0,2,8,10,16,18,24,26}
+      double af[MF], bf[NF];
+#pragma unroll
+      for (int i = 0; i < MF; ++i) af[i] = as[tma_off<AKM>(wm0 + i * 8 + gq, kp)];
+#pragma unroll
+      for (int j = 0; j < NF; ++j) bf[j] = bs[tma_off<BKM>(wn0 + j * 8 + gq, kp)];
+#pragma unroll
+      for (int i = 0; i < MF; ++i)
+#pragma unroll
+        for (int j = 0; j < NF; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
+  }
+  __syncthreads();
+}
+
+}  // namespace stbta
