@@ -14,17 +14,18 @@ value  = algorithmic FLOPs of the three routines (SURVEY.md §8(d) formulas,
 e2e    = the same metric through the reference-facing Python API with HOST
          buffers: pinned matrix upload, factorize, logdet read-back, solve
          of a host RHS, selected inverse copied back to pinned host memory.
-roofline: the dominant routine (POBTAF, a chain of DMMA launches on one
-         stream) against the FP64 DMMA peak measured live on the box with a
+roofline: the dominant routine (the longest of POBTAF / POBTASI, each a short
+         chain of launches on one stream) against the FP64 DMMA peak measured live on the box with a
          register-resident DMMA.8x8x4 loop (MEASURED_PEAKS.json has no FP64
          entry).
 cpu_baseline: the oracle port of the reference algorithm (numpy/OpenBLAS,
          oracle/bta_np.py) on a bounded sample, rank 0 at N=1 only.
 
-Multi-GPU (torchrun): every rank factorizes its own C2 replica — the BTA
-solve of one matrix has no data-parallel split until the S3 distributed
-solver lands — so scaling is "weak" and there is no collective on
-the data path; only the timing max-reduction uses NCCL.
+Multi-GPU (torchrun): every rank factorizes its own C2 replica (the C2
+microbench is one matrix per GPU), so scaling is "weak" and there is no
+collective on the data path; only the timing max-reduction uses NCCL.  The
+time-partitioned distributed solver (S3, NCCL point-to-point reduced system)
+is measured with `--config c5` (SURVEY §8(d) C5, 96 time blocks per GPU).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
 """
@@ -436,16 +437,26 @@ def main():
         inla_obj = measure_c3(dev)
 
     if rank == 0:
-        achieved = f_f / t_f / 1e12
+        # roofline of the dominant routine (the longest launch chain of the step)
+        dom = "pobtasi" if t_i > t_f else "pobtaf"
+        achieved = (f_i / t_i if dom == "pobtasi" else f_f / t_f) / 1e12
+        traffic = None
+        tpath = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01_traffic.json")
+        if os.path.exists(tpath) and (n, b, a) == (48, 2048, 6):
+            with open(tpath) as fh:
+                traffic = json.load(fh).get(f"c2_{dom}", {}).get("dram_bytes")
+        kname = ("POBTASI (stbta_pobtasi launch chain: W pre-pass + persistent TMA recursion)"
+                 if dom == "pobtasi" else "POBTAF (stbta_pobtaf launch chain: persistent TMA task graph)")
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (reference generator law: SPD L L^T, seeded, drawn on device)",
             "config": workload(args),
-            "roofline": {"bound": "tensor", "kernel": "POBTAF (stbta_pobtaf launch chain)",
+            "roofline": {"bound": "tensor", "kernel": kname,
                          "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                         "frac": achieved / peak, "traffic": None,
+                         "frac": achieved / peak, "traffic": traffic,
+                         "traffic_unit": "DRAM bytes per call (ncu, profiles/r01_traffic.json)",
                          "peak_source": "FP64 DMMA.8x8x4 register-loop probe measured live "
                                         "(MEASURED_PEAKS.json has no FP64 entry)"},
             "routines": {
