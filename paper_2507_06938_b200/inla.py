@@ -614,14 +614,37 @@ def minimize(objective, theta0, gtol=1e-3, ftol=1e-6, max_iter=100, grad_step=1e
             direction = -grad
             slope = -float(grad @ grad)
         step, accepted, tries = 1.0, False, 0
-        for _ in range(max_backtracks + 1):
+        width = int(getattr(runner, "width", 1)) if runner is not None else 1
+        if width > 1:
+            # Armijo backtracking with the next `width` step sizes evaluated
+            # concurrently (one per GPU); the first acceptable one in
+            # backtracking order is taken, so the accepted step, theta and
+            # the sequential try count are exactly those of the loop below.
+            k, st = 0, 1.0
+            while k <= max_backtracks and not accepted:
+                ks = list(range(k, min(k + width, max_backtracks + 1)))
+                steps = []
+                for _ in ks:  # the same repeated products as the sequential loop
+                    steps.append(st)
+                    st *= shrink
+                vals = _run(fun, [theta + sj * direction for sj in steps], runner)
+                for j, sj, fv in zip(ks, steps, vals):
+                    if np.isfinite(fv) and fv <= f + c1 * sj * slope:
+                        step, accepted, tries = sj, True, j + 1
+                        break
+                k = ks[-1] + 1
+            if not accepted:
+                tries = max_backtracks + 1
             cand = theta + step * direction
-            f_cand = fun(cand)
-            tries += 1
-            if np.isfinite(f_cand) and f_cand <= f + c1 * step * slope:
-                accepted = True
-                break
-            step *= shrink
+        else:
+            for _ in range(max_backtracks + 1):
+                cand = theta + step * direction
+                f_cand = fun(cand)
+                tries += 1
+                if np.isfinite(f_cand) and f_cand <= f + c1 * step * slope:
+                    accepted = True
+                    break
+                step *= shrink
         n_eval += tries
         if not accepted:
             status = "line_search_failed"

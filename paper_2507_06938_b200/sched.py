@@ -148,6 +148,20 @@ class GpuRunner:
         self.negate = negate
         self.trace = trace
         self.depth = max(1, int(depth))
+        # one long-lived worker thread per GPU, always driving the same
+        # evaluator: workspace slots are keyed by thread, so fresh (or
+        # rotating) threads would allocate fresh Q_p / Q_c workspaces
+        self._pools = None
+
+    @property
+    def width(self):
+        """Evaluations that run concurrently (one per GPU)."""
+        return len(self.evaluators)
+
+    def close(self):
+        for p in self._pools or []:
+            p.shutdown(wait=True)
+        self._pools = None
 
     @staticmethod
     def _point(task):
@@ -179,8 +193,11 @@ class GpuRunner:
         if G == 1:
             worker(0)
         else:
-            with ThreadPoolExecutor(max_workers=G) as pool:
-                list(pool.map(worker, range(G)))
+            if self._pools is None:
+                self._pools = [ThreadPoolExecutor(max_workers=1) for _ in range(G)]
+            futs = [self._pools[g].submit(worker, g) for g in range(G)]
+            for f in futs:
+                f.result()
         if failures:
             idx, exc = min(failures, key=lambda p: p[0])
             raise TaskError(idx, str(exc)) from exc
@@ -203,6 +220,10 @@ class DistRunner:
         self.negate = negate
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
+
+    @property
+    def width(self):
+        return self.world
 
     def evaluate_points(self, points):
         import torch

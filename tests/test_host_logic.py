@@ -180,3 +180,36 @@ def test_padded_offsets_roundtrip():
         sel[off] = True
         np.testing.assert_array_equal(back[sel], flat[sel])
         assert np.all(np.diff(poff) > 0)
+
+
+def test_parallel_line_search_matches_sequential():
+    """Batched Armijo backtracking (one candidate step per GPU) takes the same
+    steps, iterates and try counts as the reference's sequential loop."""
+    import numpy as np
+    from paper_2507_06938_b200 import inla
+
+    def rosen(x):
+        x = np.asarray(x)
+        return float(np.sum(100.0 * (x[1:] - x[:-1] ** 2) ** 2 + (1 - x[:-1]) ** 2))
+
+    class Runner:
+        def __init__(self, width):
+            self.width = width
+            self.calls = 0
+
+        def __call__(self, tasks):
+            self.calls += 1
+            return [t() for t in tasks]
+
+    x0 = np.array([-1.2, 1.0, 0.5, -0.3])
+    seq = inla.minimize(rosen, x0, gtol=1e-6, ftol=1e-14, max_iter=60)
+    for width in (2, 3, 8):
+        r = Runner(width)
+        rec_s, rec_p = [], []
+        inla.minimize(rosen, x0, gtol=1e-6, ftol=1e-14, max_iter=60, on_iteration=rec_s.append)
+        par = inla.minimize(rosen, x0, gtol=1e-6, ftol=1e-14, max_iter=60, runner=r,
+                            on_iteration=rec_p.append)
+        assert par.theta.tolist() == seq.theta.tolist() and par.f == seq.f
+        assert par.iterations == seq.iterations
+        assert [(a.step, a.f_evals) for a in rec_p] == [(a.step, a.f_evals) for a in rec_s]
+    assert any(a.step < 1.0 for a in rec_s)  # the path does backtrack
