@@ -10,6 +10,8 @@
 // 8x4 fragment reads conflict-free without padding.  Rows beyond the tile
 // (partial tiles) come in as whatever lies there and only feed output rows /
 // columns the caller does not store; columns >= the tensor width read as zero.
+// The k-steps read the slab columns in the permuted order of tma_kp(), which
+// keeps the fragment reads conflict-free.
 #pragma once
 
 #include <cuda.h>
@@ -37,6 +39,27 @@ STBTA_DEV void tma_load_2d(double* dst, const CUtensorMap* map, int col, int row
       " [%0], [%1, {%2, %3}], [%4];\n" ::"r"(smem_u32(dst)),
       "l"(reinterpret_cast<unsigned long long>(map)), "r"(col), "r"(row), "r"(smem_u32(bar))
       : "memory");
+}
+
+// Offset of element (r, kp) of one operand's 32-wide slab (r = rb + gq, rb % 8
+// == 0): row-major operands are two 16 x 128 boxes, k-major ones eight 16 x 32
+// boxes, both 128-byte swizzled (16-byte chunk index ^= 128-byte row & 7).
+template <bool KM>
+STBTA_DEV int tma_off(int r, int kp) {
+  if (!KM) return (kp >> 4) * TMA_HALF + r * 16 + ((((kp & 15) >> 1) ^ (r & 7)) << 1) + (kp & 1);
+  return (r >> 4) * 512 + kp * 16 + ((((r & 15) >> 1) ^ (kp & 7)) << 1) + (r & 1);
+}
+
+// Physical slab column read by k-step ks (0..7) in lane quad position tq:
+// kp = KB[ks] ^ O[tq], KB = {0,1,4,5,16,17,20,21}, O = {0,3,12,15} -- a
+// permutation of 0..31 (the same for A and B, so the product is unchanged)
+// under which every 64-bit fragment read is conflict-free in BOTH layouts:
+// each half-warp (4 rows x 4 quads) must hit 16 distinct bank pairs, which
+// needs kp bits {0,3} (row-major) and {1,2} (k-major) to take all four values
+// across the quad (checked exhaustively in tests/test_host_logic.py).
+// o4 = O[tq] = (tq & 1) * 3 + (tq >> 1) * 12.
+STBTA_DEV int tma_kp(int ks, int o4) {
+  return ((ks & 1) + ((ks >> 1) & 1) * 4 + (ks >> 2) * 16) ^ o4;
 }
 
 // 1 KB-aligned staging base inside `smem` (128-byte swizzle atoms are 1 KB).
@@ -85,10 +108,7 @@ STBTA_DEV void tile_mma_tma(double (&acc)[Cfg::MF][Cfg::NF][2], const TmaOpnd& A
       if (s < nk) issue(s);
   }
   init();
-  // per-lane swizzled offsets: element (r, k) of a box at r*16 + (((k>>1) ^ (r&7)) << 1) + (k&1)
-  int swz[4];
-#pragma unroll
-  for (int c = 0; c < 4; ++c) swz[c] = ((((c * 2) + (tq >> 1)) ^ gq) << 1) + (tq & 1);
+  const int o4 = (tq & 1) * 3 + (tq >> 1) * 12;  // see tma_kp()
   for (int kt = 0; kt < nk; ++kt) {
     const int s = kt % TMA_ST;
     mbar_wait(bars + s, (phase >> s) & 1u);
@@ -99,13 +119,13 @@ STBTA_DEV void tile_mma_tma(double (&acc)[Cfg::MF][Cfg::NF][2], const TmaOpnd& A
     const double* bs = as + TMA_OPND;
 #pragma unroll
     for (int ks = 0; ks < 8; ++ks) {
-      const int h = (ks >> 2) * TMA_HALF, o = swz[ks & 3];
+      const int kp = tma_kp(ks, o4);
       double af[MF], bf[NF];
 #pragma unroll
-      for (int i = 0; i < MF; ++i) af[i] = as[h + (wm0 + i * 8 + gq) * 16 + o];
+      for (int i = 0; i < MF; ++i) af[i] = as[tma_off<false>(wm0 + i * 8 + gq, kp)];
 #pragma unroll
       for (int j = 0; j < NF; ++j) {
-        const double bv = bs[h + (wn0 + j * 8 + gq) * 16 + o];
+        const double bv = bs[tma_off<false>(wn0 + j * 8 + gq, kp)];
         bf[j] = NEG ? -bv : bv;
       }
 #pragma unroll
@@ -158,13 +178,6 @@ STBTA_DEV void tma_issue_opnd(double* dst, const TmaOpnd3& o, int k0, unsigned l
   }
 }
 
-// offset of element (r, kp) of one operand's slab; r = rb + gq with rb % 8 == 0
-template <bool KM>
-STBTA_DEV int tma_off(int r, int kp) {
-  if (!KM) return (kp >> 4) * TMA_HALF + r * 16 + ((((kp & 15) >> 1) ^ (r & 7)) << 1) + (kp & 1);
-  return (r >> 4) * 512 + kp * 16 + ((((r & 15) >> 1) ^ (kp & 7)) << 1) + (r & 1);
-}
-
 // acc += A * B^T over k in [kbeg, K), (K - kbeg) % 32 == 0.
 template <class Cfg, bool AKM, bool BKM>
 STBTA_DEV void tile_mma_tma3(double (&acc)[Cfg::MF][Cfg::NF][2], const TmaOpnd3& A,
@@ -191,7 +204,7 @@ STBTA_DEV void tile_mma_tma3(double (&acc)[Cfg::MF][Cfg::NF][2], const TmaOpnd3&
     for (int s = 0; s < TMA_ST - 1; ++s)
       if (s < nk) issue(s);
   }
-  const int o4 = (tq & 1) + 4 * (tq >> 1);  // {0, 1, 4, 5}
+  const int o4 = (tq & 1) * 3 + (tq >> 1) * 12;  // see tma_kp()
   for (int kt = 0; kt < nk; ++kt) {
     const int s = kt % TMA_ST;
     mbar_wait(bars + s, (phase >> s) & 1u);
@@ -202,7 +215,7 @@ STBTA_DEV void tile_mma_tma3(double (&acc)[Cfg::MF][Cfg::NF][2], const TmaOpnd3&
     const double* bs = as + TMA_OPND;
 #pragma unroll
     for (int ks = 0; ks < 8; ++ks) {
-      const int kp = (ks >> 1) * 8 + (ks & 1) * 2 + o4;  // KB = {0,2,8,10,16,18,24,26}
+      const int kp = tma_kp(ks, o4);
       double af[MF], bf[NF];
 #pragma unroll
       for (int i = 0; i < MF; ++i) af[i] = as[tma_off<AKM>(wm0 + i * 8 + gq, kp)];

@@ -213,3 +213,27 @@ def test_parallel_line_search_matches_sequential():
         assert par.iterations == seq.iterations
         assert [(a.step, a.f_evals) for a in rec_p] == [(a.step, a.f_evals) for a in rec_s]
     assert any(a.step < 1.0 for a in rec_s)  # the path does backtrack
+
+
+def test_tma_fragment_order_is_conflict_free_permutation():
+    """tma_mma.cuh: the k-step column order kp = KB[ks] ^ O[tq] is a
+    permutation of the 32 slab columns, and every 64-bit DMMA fragment read
+    (processed per half-warp: 16 lanes must hit 16 distinct bank pairs) is
+    conflict-free in both the row-major and the k-major 128B-swizzled layouts."""
+    def rm_off(r, kp):  # tma_off<false>
+        return (kp >> 4) * 2048 + r * 16 + ((((kp & 15) >> 1) ^ (r & 7)) << 1) + (kp & 1)
+
+    def km_off(r, kp):  # tma_off<true>
+        return (r >> 4) * 512 + kp * 16 + ((((r & 15) >> 1) ^ (kp & 7)) << 1) + (r & 1)
+
+    def kp_of(ks, tq):  # tma_kp
+        o4 = (tq & 1) * 3 + (tq >> 1) * 12
+        return ((ks & 1) + ((ks >> 1) & 1) * 4 + (ks >> 2) * 16) ^ o4
+
+    assert sorted(kp_of(ks, tq) for ks in range(8) for tq in range(4)) == list(range(32))
+    for off in (rm_off, km_off):
+        for ks in range(8):
+            for base in range(0, 128, 8):
+                addrs = [off(base + (lane >> 2), kp_of(ks, lane & 3)) for lane in range(32)]
+                for half in (addrs[:16], addrs[16:]):
+                    assert len({a % 16 for a in half}) == 16  # distinct bank pairs
