@@ -28,10 +28,13 @@ namespace stbta {
 constexpr int PS_NT = 256;
 constexpr int NR = 8;      // right-hand sides per sweep launch
 constexpr int SL = 32;     // slice width
-constexpr int PST = 3;     // ring stages
-constexpr int F_LD = SL + 1;           // forward slice: 128 rows x 32 cols
-constexpr int B_LD = 128 + 1;          // backward slice: 32 rows x 128 cols
+constexpr int PST = 4;     // ring stages
+constexpr int F_LD = SL;               // forward slice: 128 rows x 32 cols, 16-byte chunks swizzled
+constexpr int B_LD = 128;              // backward slice: 32 rows x 128 cols (read along rows)
 constexpr int STAGE = 128 * F_LD > SL * B_LD ? 128 * F_LD : SL * B_LD;
+// forward slice element (r, q): chunk (q >> 1) of row r stored at chunk (q >> 1) ^ (r & 7), so
+// the 16-byte reads of 8 consecutive rows at one chunk hit 8 distinct bank quads
+STBTA_DEV int fsw(int r, int q) { return r * F_LD + ((((q >> 1) ^ (r & 7))) << 1) + (q & 1); }
 constexpr int P_LD = 129;              // coupling block in shared memory
 constexpr int WPK = 128 * 129 / 2;     // packed lower 128 x 128
 constexpr int PS_SMEM_DOUBLES = WPK + 128 * P_LD + 128 * NR + 128 * NR;
@@ -82,7 +85,8 @@ __global__ void __launch_bounds__(PS_NT, 1) inv_tiles_kernel(Band g, double* win
   }
 }
 
-// One 32-wide slice of dependency tile k into a ring stage.
+// One 32-wide slice of dependency tile k into a ring stage (16-byte copies
+// when the rows are 16-byte aligned, zero fill outside the tile).
 template <bool FWD>
 STBTA_DEV void load_slice(double* ring_st, const Band& g, int R, int k, int sl, int extR,
                           int extK) {
@@ -91,23 +95,47 @@ STBTA_DEV void load_slice(double* ring_st, const Band& g, int R, int k, int sl, 
     // M = tile (R, k): rows r < extR, cols sl*32 + q (q < 32, < extK)
     const TilePtr t = tile_ptr(g, R, k);
     const int c0 = sl * SL;
-    for (int e = tid; e < 128 * SL; e += PS_NT) {
-      const int r = e >> 5, q = e & 31;
-      if (r < extR && c0 + q < extK)
-        cp_async8(ring_st + r * F_LD + q, t.p + (long long)r * t.ld + c0 + q, true);
-      else
-        ring_st[r * F_LD + q] = 0.0;
+    const bool vec = ((uintptr_t)t.p % 16 == 0) && (t.ld % 2 == 0);
+    if (vec) {
+      for (int e = tid; e < 128 * SL / 2; e += PS_NT) {
+        const int r = e >> 4, q = (e & 15) * 2;
+        int bytes = 0;
+        const double* src = t.p;
+        if (r < extR && c0 + q < extK) {
+          bytes = (c0 + q + 1 < extK) ? 16 : 8;
+          src = t.p + (long long)r * t.ld + c0 + q;
+        }
+        cp_async16(ring_st + fsw(r, q), src, bytes);
+      }
+    } else {
+      for (int e = tid; e < 128 * SL; e += PS_NT) {
+        const int r = e >> 5, q = e & 31;
+        const bool ok = r < extR && c0 + q < extK;
+        cp_async8(ring_st + fsw(r, q), ok ? t.p + (long long)r * t.ld + c0 + q : t.p, ok);
+      }
     }
   } else {
     // M = tile (k, R): rows sl*32 + q of tile k (q < 32, < extK), cols r < extR
     const TilePtr t = tile_ptr(g, k, R);
     const int r0 = sl * SL;
-    for (int e = tid; e < SL * 128; e += PS_NT) {
-      const int q = e >> 7, r = e & 127;
-      if (r0 + q < extK && r < extR)
-        cp_async8(ring_st + q * B_LD + r, t.p + (long long)(r0 + q) * t.ld + r, true);
-      else
-        ring_st[q * B_LD + r] = 0.0;
+    const bool vec = ((uintptr_t)t.p % 16 == 0) && (t.ld % 2 == 0);
+    if (vec) {
+      for (int e = tid; e < SL * 128 / 2; e += PS_NT) {
+        const int q = e >> 6, r = (e & 63) * 2;
+        int bytes = 0;
+        const double* src = t.p;
+        if (r0 + q < extK && r < extR) {
+          bytes = (r + 1 < extR) ? 16 : 8;
+          src = t.p + (long long)(r0 + q) * t.ld + r;
+        }
+        cp_async16(ring_st + q * B_LD + r, src, bytes);
+      }
+    } else {
+      for (int e = tid; e < SL * 128; e += PS_NT) {
+        const int q = e >> 7, r = e & 127;
+        const bool ok = r0 + q < extK && r < extR;
+        cp_async8(ring_st + q * B_LD + r, ok ? t.p + (long long)(r0 + q) * t.ld + r : t.p, ok);
+      }
     }
   }
 }
@@ -224,9 +252,9 @@ __global__ void __launch_bounds__(PS_NT, 1) sweep_kernel(SweepArgs p) {
       __syncthreads();
       const long long krow0 = (long long)(k / g.nbt) * g.b + (long long)(k % g.nbt) * 128;
       const int extK = tile_extent(g, k);
-      for (int e = tid; e < 128 * NR; e += PS_NT) {
-        const int q = e / NR, c = e % NR;
-        ybuf[e] = (q < extK && c < nc) ? __ldcg(p.x + (krow0 + q) * p.ldx + c) : 0.0;
+      for (int e = tid; e < 128 * NRC; e += PS_NT) {
+        const int q = e / NRC, c = e % NRC;
+        ybuf[q * NR + c] = (q < extK && c < nc) ? __ldcg(p.x + (krow0 + q) * p.ldx + c) : 0.0;
       }
     }
     cp_async_wait<PST - 2>();
@@ -235,12 +263,20 @@ __global__ void __launch_bounds__(PS_NT, 1) sweep_kernel(SweepArgs p) {
     const double* rs = ring + (it % PST) * STAGE;
     const int q0 = cs * SL;
 #pragma unroll 4
-    for (int qq = 0; qq < SL / 2; ++qq) {
+    for (int qq = 0; qq < SL / 2; qq += 2) {
       const int q = h * (SL / 2) + qq;
-      const double m = FWD ? rs[r * F_LD + q] : rs[q * B_LD + r];
+      double m0, m1;
+      if (FWD) {
+        const double2 v = *reinterpret_cast<const double2*>(rs + fsw(r, q));
+        m0 = v.x;
+        m1 = v.y;
+      } else {
+        m0 = rs[q * B_LD + r];
+        m1 = rs[(q + 1) * B_LD + r];
+      }
       const double* yq = ybuf + (q0 + q) * NR;
 #pragma unroll
-      for (int c = 0; c < NRC; ++c) acc[c] = fma(-m, yq[c], acc[c]);
+      for (int c = 0; c < NRC; ++c) acc[c] = fma(-m1, yq[NR + c], fma(-m0, yq[c], acc[c]));
     }
     if (++cs == nsl(k)) { cs = 0; ++cd; }
   }
