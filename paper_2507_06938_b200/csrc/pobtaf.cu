@@ -481,16 +481,38 @@ __global__ void __launch_bounds__(DAG_NT, 1) pobtaf_dag_kernel(Band g, DagWs ws,
         const TilePtr xp = tile_ptr(g, tk.R, s);
         const TilePtr lp = tile_ptr(g, s, s);
         double* Xg = xp.p + (long long)r0 * xp.ld;
-        for (int e = tid; e < 32 * 128; e += DAG_NT) {
-          const int r = e >> 7, c = e & 127;
-          if (r < rows && c < w) cp_async8(X + r * XLD + c, Xg + (long long)r * xp.ld + c, true);
-          else X[r * XLD + c] = 0.0;
+        const bool xv = ((uintptr_t)Xg % 16 == 0) && (xp.ld % 2 == 0);
+        const bool lv = ((uintptr_t)lp.p % 16 == 0) && (lp.ld % 2 == 0);
+        if (xv) {  // 16-byte copies (zero fill past the tile)
+          for (int e = tid; e < 32 * 64; e += DAG_NT) {
+            const int r = e >> 6, c = (e & 63) * 2;
+            const int bytes = (r < rows && c < w) ? ((c + 1 < w) ? 16 : 8) : 0;
+            cp_async16(X + r * XLD + c, bytes ? Xg + (long long)r * xp.ld + c : Xg, bytes);
+          }
+        } else {
+          for (int e = tid; e < 32 * 128; e += DAG_NT) {
+            const int r = e >> 7, c = e & 127;
+            if (r < rows && c < w) cp_async8(X + r * XLD + c, Xg + (long long)r * xp.ld + c, true);
+            else X[r * XLD + c] = 0.0;
+          }
         }
-        for (int e = tid; e < 128 * 128; e += DAG_NT) {
-          const int r = e >> 7, c = e & 127;
-          if ((r >> 5) > (c >> 5)) {  // strictly-lower 32-blocks
-            if (r < w && c < w) cp_async8(Ls + r * TLD + c, lp.p + (long long)r * lp.ld + c, true);
-            else Ls[r * TLD + c] = 0.0;
+        if (lv) {  // strictly-lower 32-blocks: 6 blocks of 32 x 32
+          for (int e = tid; e < 6 * 32 * 16; e += DAG_NT) {
+            // blocks (1,0) (2,0) (2,1) (3,0) (3,1) (3,2)
+            const int blk = e >> 9, rr = (e >> 4) & 31, cc = (e & 15) * 2;
+            const int br = blk < 1 ? 1 : (blk < 3 ? 2 : 3);
+            const int bc = blk - br * (br - 1) / 2;
+            const int r = br * 32 + rr, c = bc * 32 + cc;
+            const int bytes = (r < w && c < w) ? ((c + 1 < w) ? 16 : 8) : 0;
+            cp_async16(Ls + r * TLD + c, bytes ? lp.p + (long long)r * lp.ld + c : lp.p, bytes);
+          }
+        } else {
+          for (int e = tid; e < 128 * 128; e += DAG_NT) {
+            const int r = e >> 7, c = e & 127;
+            if ((r >> 5) > (c >> 5)) {  // strictly-lower 32-blocks
+              if (r < w && c < w) cp_async8(Ls + r * TLD + c, lp.p + (long long)r * lp.ld + c, true);
+              else Ls[r * TLD + c] = 0.0;
+            }
           }
         }
         const double* Wg = ws.W + (long long)s * W_SLOT;
