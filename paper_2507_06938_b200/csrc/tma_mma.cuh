@@ -1,7 +1,8 @@
 // TMA-staged variant of tile_mma for 128 x 128 tiles whose operands are both
 // K-contiguous row sets of a region described by a CUtensorMap (POBTAF UPDATE):
 //
-//   acc(128 x 128) (+)= A(128 x K) * B(128 x K)^T,   K % 32 == 0
+//   acc(128 x 128) (+)= A(128 x K) * B(128 x K)^T,   K % 32 == 0 or the K range
+//   ending at the tensor's last column (the partial slab is zero-filled)
 //
 // Thread 0 streams each 32-wide K slab of A and B with four
 // cp.async.bulk.tensor.2d copies (16 x 128 boxes, 128-byte swizzle) onto a
@@ -89,7 +90,7 @@ STBTA_DEV void tile_mma_tma(double (&acc)[Cfg::MF][Cfg::NF][2], const TmaOpnd& A
   const int gq = lane >> 2, tq = lane & 3;
   const int wm0 = (warp % Cfg::WARPS_M) * Cfg::WM;
   const int wn0 = (warp / Cfg::WARPS_M) * Cfg::WN;
-  const int nk = K / 32;
+  const int nk = (K + 31) / 32;  // a partial last slab must end at the tensor edge (zero fill)
   auto issue = [&](int kt) {  // thread 0
     double* st = base + (kt % TMA_ST) * TMA_STAGE;
     unsigned long long* bar = bars + kt % TMA_ST;
