@@ -47,19 +47,22 @@ constexpr int DAG_SMEM_DOUBLES =
 constexpr int W_SLOT = 4 * 32 * 32;  // per panel: the four W_kk^T blocks
 constexpr size_t DAG_SMEM_BYTES = DAG_SMEM_DOUBLES * sizeof(double);
 
-// Ticket order, six groups per panel s (critical chain first, then the bulk
-// of the previous panel, then this panel's remaining TRSMs and column s+1):
+// Ticket order, eight groups per panel s (the critical chain first, then the
+// second-row look-ahead, then the bulk of the previous panel, then this
+// panel's remaining TRSMs and column s+1):
 //   G0 TRSM(s, s+1, q)          the next diagonal tile's strips   [critical]
 //   G1 STRIP(s-1, s+1, q)       previous panel's update of that tile
 //   G2 STRIP(s, s+1, q)         this panel's update of it  -> POTRF(s+1)
-//   G3 E(s-1) \ G1              bulk updates of panel s-1, columns >= s+1
-//   G4 TRSM(s, R, q), R > s+1
-//   G5 UPDATE(s, R, s+1), R > s+1
+//   G3 TRSM(s, r1, q)           r1 = second band row (= s+2 inside a block)
+//   G4 UPDATE(s-1, r1, s+1), UPDATE(s, r1, s+1)   -> TRSM(s+1, r1) = G0(s+1)
+//   G5 E(s-1) \ (G1, G4)        bulk updates of panel s-1, columns >= s+1
+//   G6 TRSM(s, R, q), R beyond r1
+//   G7 UPDATE(s, R, s+1), R beyond r1
 // Every task depends only on tasks of earlier groups (or the panel worker's
 // POTRF, which depends only on earlier groups), so ticket order is a
 // topological order and spinning never deadlocks.
 enum { T_POTRF = 0, T_TRSM = 1, T_UPD = 2, T_STRIP = 3 };
-constexpr int NGRP = 6;
+constexpr int NGRP = 8;
 constexpr int PROF_TL = 64;  // debug profile: per-panel timeline (12 slots) from here
 struct DagWs {
   int* gstart;   // G + 1 group starts
@@ -135,17 +138,32 @@ STBTA_DEV bool cross_col(const Band& g, int p, int C) {
   return C >= chunk_end(g, p) + 1 + look(g);
 }
 
+// Does panel p = s-1 update tile (r1, s+1), r1 = second band row of s?  Then
+// that update is hoisted from the bulk (G5) to the front of G4, ahead of
+// panel s's own update of the tile (never chunked: its column is s+1).
+STBTA_DEV bool g4_prev(const Band& g, int s) {
+  if (s < 1 || s >= g.SP) return false;
+  int mb, mbp;
+  const int m = band_rows(g, s, &mb);
+  if (m < 2) return false;
+  const int mp = band_rows(g, s - 1, &mbp);
+  return mp >= 3 && band_row(g, s - 1, 1, mbp) == s + 1 &&
+         band_row(g, s - 1, 2, mbp) == band_row(g, s, 1, mb);
+}
+
 STBTA_DEV int group_size(const Band& g, int kind, int s) {
   int mb;
-  if (s >= g.SP) {  // trailing groups: only the last eliminated panel's bulk (G1, G3)
-    if (kind != 1 && kind != 3) return 0;
+  if (s >= g.SP) {  // trailing groups: only the last eliminated panel's bulk (G1, G5)
+    if (kind != 1 && kind != 5) return 0;
   }
   const int m = s < g.S ? band_rows(g, s, &mb) : 0;
   switch (kind) {
     case 0: return m >= 1 ? NSTRIP : 0;
     case 1: return g1_active(g, s) ? NSTRIP : 0;
     case 2: return m >= 1 ? NSTRIP : 0;
-    case 3: {
+    case 3: return m >= 2 ? NSTRIP : 0;
+    case 4: return (m >= 2 ? 1 : 0) + (g4_prev(g, s) ? 1 : 0);
+    case 5: {
       if (s < 1) return 0;
       const int p = s - 1;
       const int mp = band_rows(g, p, &mb);
@@ -155,15 +173,15 @@ STBTA_DEV int group_size(const Band& g, int kind, int s) {
         if (!last && cross_col(g, p, band_row(g, p, j, mb))) continue;
         e += NSTRIP + (mp - 1 - j);
       }
-      return e - (g1_active(g, s) ? NSTRIP : 0);
+      return e - (g1_active(g, s) ? NSTRIP : 0) - (g4_prev(g, s) ? 1 : 0);
     }
-    case 4: return m >= 1 ? NSTRIP * (m - 1) : 0;
-    default: return m >= 1 ? m - 1 : 0;
+    case 6: return m >= 3 ? NSTRIP * (m - 2) : 0;
+    default: return m >= 3 ? m - 2 : 0;
   }
 }
 
 // one extra (partial) group set after the last eliminated panel carries its bulk updates
-inline int n_groups(int SP) { return NGRP * SP + 4; }
+inline int n_groups(int SP) { return NGRP * SP + 6; }
 
 // one CTA of 1024 threads: gstart[gi] = sum of sizes of groups < gi
 __global__ void __launch_bounds__(1024) dag_setup_kernel(Band g, DagWs ws) {
@@ -219,25 +237,35 @@ STBTA_DEV Task decode(const Band& g, const DagWs& ws, int t, int lo) {
     case 0: k.type = T_TRSM; k.s = s; k.R = s + 1; k.q = local; return k;
     case 1: k.type = T_STRIP; k.s = s - 1; k.R = k.C = s + 1; k.q = local; return k;
     case 2: k.type = T_STRIP; k.s = s; k.R = k.C = s + 1; k.q = local; return k;
+    case 3:
+    case 6: {
+      int mb;
+      band_rows(g, s, &mb);
+      const int off = kind == 3 ? 1 : 2;
+      k.type = T_TRSM; k.s = s; k.R = band_row(g, s, off + local / NSTRIP, mb); k.q = local % NSTRIP;
+      return k;
+    }
     case 4: {
       int mb;
       band_rows(g, s, &mb);
-      k.type = T_TRSM; k.s = s; k.R = band_row(g, s, 1 + local / NSTRIP, mb); k.q = local % NSTRIP;
+      k.type = T_UPD; k.R = band_row(g, s, 1, mb); k.C = s + 1;
+      k.s = (local == 0 && g4_prev(g, s)) ? s - 1 : s;
       return k;
     }
-    case 5: {
+    case 7: {
       int mb;
       band_rows(g, s, &mb);
-      k.type = T_UPD; k.s = s; k.R = band_row(g, s, 1 + local, mb); k.C = s + 1;
+      k.type = T_UPD; k.s = s; k.R = band_row(g, s, 2 + local, mb); k.C = s + 1;
       return k;
     }
     default: break;
   }
-  // G3: E(p), p = s-1, columns j = 1..mp-1; column 1's strips are in G1 when active
+  // G5: E(p), p = s-1, columns j = 1..mp-1; column 1's strips are in G1 when active
   const int p = s - 1;
   int mb;
   const int mp = band_rows(g, p, &mb);
   const bool skip = g1_active(g, s);
+  const int hoist = g4_prev(g, s) ? 1 : 0;  // UPDATE(p, band_row 2, band_row 1) is in G4
   const bool last = chunk_last(g, p);
   k.s = p;
   for (int j = 1; j < mp; ++j) {
@@ -246,11 +274,12 @@ STBTA_DEV Task decode(const Band& g, const DagWs& ws, int t, int lo) {
     if (cross && !last) continue;
     k.s0 = cross ? chunk_first(g, p) : p;
     const int ns = (j == 1 && skip) ? 0 : NSTRIP;
-    const int cnt = ns + (mp - 1 - j);
+    const int hj = j == 1 ? hoist : 0;
+    const int cnt = ns + (mp - 1 - j) - hj;
     if (local < cnt) {
       if (local < ns) { k.type = T_STRIP; k.R = k.C = c; k.q = local; return k; }
       k.type = T_UPD;
-      k.R = band_row(g, p, j + 1 + (local - ns), mb);
+      k.R = band_row(g, p, j + 1 + hj + (local - ns), mb);
       k.C = c;
       return k;
     }
