@@ -639,6 +639,12 @@ __global__ void __launch_bounds__(DAG_NT, 1) pobtaf_dag_kernel(Band g, DagWs ws,
       }
       if (tk.type == T_STRIP && tk.R == tk.s + 2 && tk.s + 2 < g.SP)
         atomicMax(ws.prof + PROF_TL + (long long)(tk.s + 1) * 12 + 9, t2);
+      // updates of tile (C+1, C) (the tile TRSM(C, C+1) solves): slot 10 = claim of the
+      // latest one, slot 11 = its completion, for panel C
+      if (tk.type == T_UPD && tk.R == tk.C + 1 && tk.C < g.SP) {
+        atomicMax(ws.prof + PROF_TL + (long long)tk.C * 12 + 10, t0);
+        atomicMax(ws.prof + PROF_TL + (long long)tk.C * 12 + 11, t2);
+      }
       atomicAdd(ws.prof + 3 * tk.type, 1ull);
       atomicAdd(ws.prof + 3 * tk.type + 1, t1 - t0);
       atomicAdd(ws.prof + 3 * tk.type + 2, t2 - t1);

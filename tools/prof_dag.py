@@ -48,3 +48,5 @@ print("critical chain per panel (us): potrf exec %.2f | potrf_end -> trsm deps o
 print("claims: trsm claimed %.2f us before potrf end, strip claimed %.2f us before trsm end; G1 strip end - potrf_end(s) %.2f us; next potrf t1 - g1 end %.2f" % (
     avg(lambda s: tl[s,2]-tl[s,3]), avg(lambda s: tl[s,5]-tl[s,6]), avg(lambda s: tl[s,9]-tl[s,2]), avg(lambda s: tl[s+1,1]-tl[s,9])))
 print("panel period %.2f us" % avg(lambda s: tl[s+1,2]-tl[s,2]))
+print("tile (s+1,s) last prior update: claimed %.2f us, done %.2f us relative to POTRF(s) end" % (
+    avg(lambda s: tl[s,10]-tl[s,2]), avg(lambda s: tl[s,11]-tl[s,2])))
