@@ -378,12 +378,15 @@ STBTA_DEV bool potrf_worker(const Band& g, const DagWs& ws, int* info, double* s
         }
         return false;
       }
-      // L (zero strict upper) back to the tile, W_kk^T blocks to the panel's slot
+      // First what the TRSM tasks read: the strictly-lower 32-blocks of L and
+      // the W_kk^T blocks; the diagonal 32-blocks and the zero upper part are
+      // stored after the signal (nobody reads them inside the kernel).
       {
         const int warp = tid >> 5, lane = tid & 31;
-        for (int r = warp; r < w; r += DAG_NT / 32) {
+        for (int r = 32 + warp; r < w; r += DAG_NT / 32) {
           double* dst = tp.p + (long long)r * tp.ld;
-          for (int c = lane; c < w; c += 32) dst[c] = (c <= r) ? T[r * PT_LD + c] : 0.0;
+          const int cend = min(w, r & ~31);
+          for (int c = lane; c < cend; c += 32) dst[c] = T[r * PT_LD + c];
         }
       }
       double* Wg = ws.W + (long long)s * W_SLOT;
@@ -409,6 +412,13 @@ STBTA_DEV bool potrf_worker(const Band& g, const DagWs& ws, int* info, double* s
           atomicAdd(ws.prof + 2, tend - t1);
           unsigned long long* tlp = ws.prof + PROF_TL + (long long)s * 12;
           tlp[0] = t0; tlp[1] = t1; tlp[2] = tend;
+        }
+      }
+      {  // the rest of the tile: diagonal 32-blocks of L and zeros above them
+        const int warp = tid >> 5, lane = tid & 31;
+        for (int r = warp; r < w; r += DAG_NT / 32) {
+          double* dst = tp.p + (long long)r * tp.ld;
+          for (int c = (r & ~31) + lane; c < w; c += 32) dst[c] = (c <= r) ? T[r * PT_LD + c] : 0.0;
         }
       }
     }
