@@ -2,7 +2,7 @@
 set -e
 cd /root/repo/paper_2507_06938_b200/csrc
 cp pobtaf.cu /tmp/pobtaf_orig.cu
-for cfg in "2 3 8 4" "2 3 16 8" "2 2 16 8" "3 3 8 4" "2 3 12 6"; do
+for cfg in "2 3 8 4" "2 3 16 4" "2 3 12 4" "3 3 16 4" "2 3 24 4"; do
   set -- $cfg
   cp /tmp/pobtaf_orig.cu pobtaf.cu
   sed -i "s/^STBTA_DEV int look(const Band\& g) { return g.nbt >= 24 ? [0-9]* : [0-9]*; }/STBTA_DEV int look(const Band\& g) { return g.nbt >= 24 ? $1 : $2; }/" pobtaf.cu
