@@ -234,3 +234,25 @@ def test_full_size_c2_properties(cuda):
     Q2.data.mul_(3.7)
     ld2 = bta.logdet(bta.factorize(Q2))
     np.testing.assert_allclose(ld2, (n * b + a) * np.log(3.7) + ld, rtol=1e-12)
+
+
+# Shapes that exercise the POBTAF scheduling paths: chunked updates (>= 5 tile
+# columns per block, CHUNK 4 / 8), the second-row look-ahead groups, partial
+# last tiles with and without 16-byte rows (TMA vs cp.async), TMA slabs that
+# end at the block edge, wide arrows (a > 128) and blocks of one tile.
+@pytest.mark.parametrize("n,b,a", [(4, 640, 3), (3, 1000, 0), (3, 3072, 6), (2, 1300, 131),
+                                   (5, 128, 4), (3, 897, 2), (2, 4000, 1)])
+def test_scheduling_paths_vs_oracle(cuda, n, b, a):
+    bta = _bta()
+    rng = np.random.default_rng(97 * n + b + a)
+    data = bta_np.random_spd_bta(rng, n, b, a)
+    ref = data.copy()
+    has = bta_np.factorize(ref, n, b, a)
+    m = bta.BTAMatrix(n, b, a, data)
+    f = bta.factorize(m)
+    assert f.has_arrow == has
+    np.testing.assert_allclose(m.numpy(), ref, rtol=0, atol=1e-11)
+    np.testing.assert_allclose(bta.logdet(f), bta_np.logdet(ref, n, b, a), rtol=1e-12)
+    inv = bta.selected_invert(f).numpy()
+    np.testing.assert_allclose(inv, bta_np.selected_invert(ref, n, b, a, has), rtol=1e-9,
+                               atol=1e-11)
