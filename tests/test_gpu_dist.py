@@ -36,7 +36,8 @@ def test_dist_golden_cases(cuda):
 
 
 @pytest.mark.parametrize("n,b,a,P,lb", [(12, 130, 3, 3, 1.0), (20, 64, 2, 4, 1.6), (9, 257, 0, 2, 1.0),
-                                        (16, 100, 5, 4, 1.0), (8, 33, 1, 4, 1.0)])
+                                        (16, 100, 5, 4, 1.0), (8, 33, 1, 4, 1.0),
+                                        (8, 640, 3, 2, 1.0), (9, 1100, 2, 3, 1.6)])
 def test_dist_matches_sequential(cuda, n, b, a, P, lb):
     bta, bta_dist = _mods()
     rng = np.random.default_rng(n * 7 + b + a + P)
