@@ -14,6 +14,7 @@ on the same numbers.  What changes is :class:`ObjectiveEvaluator`:
   a single host synchronisation per f_obj.
 """
 
+import itertools
 import threading
 import time
 import warnings
@@ -115,6 +116,30 @@ class ThetaPrior:
         return float(
             -0.5 * np.sum(z**2) - np.sum(np.log(self.sd)) - 0.5 * self.mean.size * LOG_2PI
         )
+
+
+# log det Q_p and pivot flag per (spec, prior coefficients), shared by the
+# evaluators of all GPUs of the process (small LRU).
+_PRIOR_CACHE = {}
+_PRIOR_ORDER = []
+_PRIOR_LOCK = threading.Lock()
+_PRIOR_MAX = 32
+_SPEC_TOKENS = itertools.count(1)
+
+
+def _prior_cache_get(key):
+    with _PRIOR_LOCK:
+        return _PRIOR_CACHE.get(key)
+
+
+def _prior_cache_put(key, logdet, info):
+    with _PRIOR_LOCK:
+        if key in _PRIOR_CACHE:
+            return
+        _PRIOR_CACHE[key] = (logdet, info)
+        _PRIOR_ORDER.append(key)
+        while len(_PRIOR_ORDER) > _PRIOR_MAX:
+            _PRIOR_CACHE.pop(_PRIOR_ORDER.pop(0), None)
 
 
 class _Scratch:
@@ -297,6 +322,22 @@ class ObjectiveEvaluator:
         cp, cc = self.assembly.coefficients(ph, linv, taus)
         return cp, cc, taus
 
+    def _spec_token(self):
+        """Identity of the model spec for the shared prior cache (a counter
+        stamped on the spec object; evaluators of the same spec share it)."""
+        tok = getattr(self.spec, "_stbta_token", None)
+        if tok is None:
+            with _PRIOR_LOCK:
+                tok = getattr(self.spec, "_stbta_token", None)
+                if tok is None:
+                    tok = next(_SPEC_TOKENS)
+                    try:
+                        setattr(self.spec, "_stbta_token", tok)
+                    except (AttributeError, TypeError):
+                        tok = ("evaluator", id(self))
+        pm = self.pmap
+        return (tok, pm.n_blocks, pm.block_size, pm.arrow_size, self.assembly.nstore)
+
     def launch(self, theta, slot=None):
         """Issue one f_obj on the device without waiting.  Returns a handle
         for :meth:`collect`, or None for a non-finite / invalid theta."""
@@ -330,10 +371,21 @@ class ObjectiveEvaluator:
             s.s_cond.wait_stream(cur)
             s.s_prior.wait_stream(cur)
             same = self.n_observations == 0
-            # prior chain (S2 layer: concurrent with the conditional chain)
+            # prior chain (S2 layer: concurrent with the conditional chain).  Its
+            # only outputs are log det Q_p and the pivot flag, a pure function of
+            # the prior coefficients: reuse them when another evaluation of the
+            # same spec already factorized this exact Q_p (e.g. the gradient
+            # stencil points that only move the noise precisions) -- the same
+            # bits, one POBTAF fewer.
+            pkey = (self._spec_token(), cp.tobytes()) if not same else None
+            cached = _prior_cache_get(pkey) if pkey is not None else None
             with torch.cuda.stream(s.s_prior):
-                self.assembly.assemble(s.ws_p, coef_p, s.s_prior)
-                self._pobtaf(s.ws_p, False, s.scal[0:1], s.info[0:1], s.s_prior)
+                if cached is not None:
+                    s.scal[0:1].fill_(cached[0])
+                    s.info[0:1].fill_(cached[1])
+                else:
+                    self.assembly.assemble(s.ws_p, coef_p, s.s_prior)
+                    self._pobtaf(s.ws_p, False, s.scal[0:1], s.info[0:1], s.s_prior)
             with torch.cuda.stream(s.s_cond):
                 if not same:
                     self.assembly.assemble(s.ws_c, coef_c, s.s_cond)
@@ -354,15 +406,17 @@ class ObjectiveEvaluator:
                 s.host_scal.copy_(s.scal, non_blocking=True)
                 s.host_info.copy_(s.info, non_blocking=True)
                 s.done.record(s.s_cond)
-        return (s, hp, taus, same)
+        return (s, hp, taus, same, pkey if cached is None else None)
 
     def collect(self, handle, want_mu=False):
         """Wait for a launched evaluation; returns (f, mu_perm_device or None)."""
         if handle is None:
             return -np.inf, None
-        s, hp, taus, same = handle
+        s, hp, taus, same, pkey = handle
         s.done.synchronize()
         info = s.host_info.numpy()
+        if pkey is not None:
+            _prior_cache_put(pkey, float(s.host_scal.numpy()[0]), int(info[0]))
         if info[0] != 0 or (not same and info[1] != 0):
             return -np.inf, None
         sc = s.host_scal.numpy()

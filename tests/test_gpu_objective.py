@@ -125,3 +125,32 @@ def test_gpu_runner_matches_serial_gradient(cuda):
     runner = sched.GpuRunner([ev], depth=2)
     f1, g1 = inla.fd_gradient(ev, theta, runner=runner)
     assert f0 == f1 and np.array_equal(g0, g1)
+
+
+def test_prior_logdet_reuse_is_bitwise_and_skips_pobtaf(cuda):
+    """Points that only move the noise precisions share Q_p: the second one
+    reuses log det Q_p (one POBTAF fewer) and its f equals a fresh evaluator's
+    bit for bit; the oracle agrees."""
+    inla = _inla()
+    from paper_2507_06938_b200 import _lib
+    lib = _lib.load()
+    nv = 2
+    spec = make_spec(nv, 3, 4, 1, 6, seed=77)
+    dim = inla.HyperParams.dim_for(nv)
+    theta = 0.05 * np.arange(dim)
+    ev = inla.ObjectiveEvaluator(spec)
+    ev.evaluate(theta)                              # fills the cache for this Q_p
+    moved = theta.copy()
+    moved[2 * nv] += 0.1                            # a noise precision (HyperParams.noise_precisions)
+    c0 = lib.stbta_launch_count()
+    f_cached, _ = ev.evaluate(moved)
+    launches_cached = lib.stbta_launch_count() - c0
+    spec2 = make_spec(nv, 3, 4, 1, 6, seed=77)      # same model, fresh spec: no cache entry
+    ev2 = inla.ObjectiveEvaluator(spec2)
+    c0 = lib.stbta_launch_count()
+    f_fresh, _ = ev2.evaluate(moved)
+    launches_fresh = lib.stbta_launch_count() - c0
+    assert f_cached == f_fresh
+    assert launches_cached < launches_fresh         # the prior assembly + POBTAF were skipped
+    fr, _ = inla_np.evaluate(spec, moved, ev.prior.mean, ev.prior.sd)
+    np.testing.assert_allclose(f_cached, fr, rtol=1e-10, atol=1e-10)
