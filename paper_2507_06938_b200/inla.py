@@ -132,6 +132,13 @@ def _prior_cache_get(key):
         return _PRIOR_CACHE.get(key)
 
 
+def prior_cache_clear():
+    """Drop the shared log det Q_p cache (benchmarks timing full evaluations)."""
+    with _PRIOR_LOCK:
+        _PRIOR_CACHE.clear()
+        _PRIOR_ORDER.clear()
+
+
 def _prior_cache_put(key, logdet, info):
     with _PRIOR_LOCK:
         if key in _PRIOR_CACHE:
