@@ -656,4 +656,6 @@ def d_selected_invert(factor, counter=None, mapper=None, phase_times=None):
             if use_arrow:
                 inv.arrow[lo:hi].copy_(Xa[:ni, ch.off :].to(dev))
             _charge(counter, b**3, ni * (2 if ch.left is not None else 1))
+            if use_arrow:  # reference bta_dist.py:584-589: a^3 per interior block
+                _charge(counter, a**3, ni)
     return inv

@@ -237,3 +237,16 @@ def test_tma_fragment_order_is_conflict_free_permutation():
                 addrs = [off(base + (lane >> 2), kp_of(ks, lane & 3)) for lane in range(32)]
                 for half in (addrs[:16], addrs[16:]):
                     assert len({a % 16 for a in half}) == 16  # distinct bank pairs
+
+
+def test_benchmark_table_writer_format(tmp_path):
+    """benchmark.write_table: one header row, floats via repr (reference
+    dataio.write_table, dataio.py:33-46)."""
+    import csv
+    from paper_2507_06938_b200 import benchmark
+
+    path = tmp_path / "t.csv"
+    benchmark.write_table(path, benchmark.HEADER, [["factorize", 1, 1.0, 4, 2, 1, "total", 0.1, 12.0]])
+    rows = list(csv.reader(open(path)))
+    assert rows[0] == benchmark.HEADER
+    assert rows[1] == ["factorize", "1", "1.0", "4", "2", "1", "total", "0.1", "12.0"]
