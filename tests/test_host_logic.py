@@ -250,3 +250,32 @@ def test_benchmark_table_writer_format(tmp_path):
     rows = list(csv.reader(open(path)))
     assert rows[0] == benchmark.HEADER
     assert rows[1] == ["factorize", "1", "1.0", "4", "2", "1", "total", "0.1", "12.0"]
+
+
+def test_output_writers_match_reference_files(tmp_path):
+    """outputs.write_summary_json / write_latent_csv / write_trace_csv produce
+    byte-identical files to the reference's dataio writers on the same
+    summary (tests/golden/outputs, oracle/make_golden_outputs.py)."""
+    import os
+    from types import SimpleNamespace
+
+    import numpy as np
+
+    from paper_2507_06938_b200 import outputs
+    from paper_2507_06938_b200.inla import HyperParams, IterationRecord, PosteriorSummary
+
+    gold = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "outputs")
+    inp = np.load(os.path.join(gold, "inputs.npz"))
+    mean, sd = inp["mean"], inp["sd"]
+    spec = SimpleNamespace(n_processes=2, n_spatial=3, n_time=2, latent_per_process=7, joint_dim=14)
+    summary = PosteriorSummary(theta_mode=HyperParams(np.linspace(-0.5, 0.5, 9), 2),
+                               theta_sd=np.linspace(0.1, 0.9, 9), latent_mean=mean, latent_sd=sd,
+                               logpost_at_mode=-123.456789, iterations=7, f_evals=321,
+                               status="converged (gradient)", theta_hessian=np.eye(9))
+    outputs.write_summary_json(tmp_path / "summary.json", summary, extra={"seed": 5})
+    outputs.write_latent_csv(tmp_path / "latent.csv", spec, mean, sd)
+    outputs.write_trace_csv(tmp_path / "trace.csv",
+                            [IterationRecord(1, -100.5, 3.25, 0.5, 40, 0.125),
+                             IterationRecord(2, -120.25, 0.5, 1.0, 32, 0.0625)])
+    for name in ("summary.json", "latent.csv", "trace.csv"):
+        assert open(tmp_path / name).read() == open(os.path.join(gold, name)).read(), name
