@@ -279,3 +279,38 @@ def test_output_writers_match_reference_files(tmp_path):
                              IterationRecord(2, -120.25, 0.5, 1.0, 32, 0.0625)])
     for name in ("summary.json", "latent.csv", "trace.csv"):
         assert open(tmp_path / name).read() == open(os.path.join(gold, name)).read(), name
+
+
+def test_model_from_files_roundtrip(tmp_path):
+    """File-based model ingestion (reference config.py:245-285): writing a
+    synthetic model's matrices as Matrix Market / CSV and reading them back
+    gives the same ModelSpec content."""
+    import numpy as np
+    import scipy.sparse as sp
+    from scipy.io import mmwrite
+
+    from conftest import make_spec
+
+    from paper_2507_06938_b200 import outputs
+
+    spec = make_spec(2, 3, 2, 1, 10, seed=5)
+    files = {k: [] for k in ("sm", "sg", "tm", "tc", "ts", "A", "y")}
+    for i in range(spec.n_processes):
+        for key, mat in (("sm", spec.spatial[i].mass), ("sg", spec.spatial[i].stiffness),
+                         ("tm", spec.temporal[i].mass), ("tc", spec.temporal[i].coupling),
+                         ("ts", spec.temporal[i].stiffness), ("A", spec.design[i])):
+            p = tmp_path / f"{key}{i}.mtx"
+            mmwrite(str(p), sp.coo_matrix(mat))
+            files[key].append(p)
+        p = tmp_path / f"y{i}.csv"
+        np.savetxt(p, np.asarray(spec.observations[i]), fmt="%.17g")
+        files["y"].append(p)
+    got = outputs.model_from_files(spec.n_processes, spec.n_spatial, spec.n_time, spec.n_fixed,
+                                   files["sm"], files["sg"], files["tm"], files["tc"], files["ts"],
+                                   files["A"], files["y"], spec.fixed_effect_precision)
+    for i in range(spec.n_processes):
+        assert (got.spatial[i].mass != spec.spatial[i].mass).nnz == 0
+        assert (got.temporal[i].coupling != spec.temporal[i].coupling).nnz == 0
+        assert (got.design[i] != sp.csr_matrix(spec.design[i])).nnz == 0
+        assert np.array_equal(got.observations[i], np.asarray(spec.observations[i]))
+    assert got.joint_dim == spec.joint_dim
