@@ -132,6 +132,18 @@ def _prior_cache_get(key):
         return _PRIOR_CACHE.get(key)
 
 
+def _prior_cache_wait(key, timeout=600.0):
+    """Block until `key` is in the prior cache (published by prior_logdet)."""
+    t0 = time.perf_counter()
+    while True:
+        hit = _prior_cache_get(key)
+        if hit is not None:
+            return hit
+        if time.perf_counter() - t0 > timeout:
+            raise TimeoutError("prior log-determinant was never published")
+        time.sleep(0.0005)
+
+
 def prior_cache_clear():
     """Drop the shared log det Q_p cache (benchmarks timing full evaluations)."""
     with _PRIOR_LOCK:
@@ -345,9 +357,51 @@ class ObjectiveEvaluator:
         pm = self.pmap
         return (tok, pm.n_blocks, pm.block_size, pm.arrow_size, self.assembly.nstore)
 
-    def launch(self, theta, slot=None):
+    def prior_logdet(self, theta, slot=None):
+        """(log det Q_p, pivot flag) at theta -- the prior half of an f_obj,
+        published to the shared prior cache (so an evaluation of the same theta
+        on another GPU launched with ``defer_prior=True`` picks it up).  Returns
+        None for an invalid theta."""
+        hp = self._hypers(theta)
+        if not np.all(np.isfinite(hp.values)) or self.n_observations == 0:
+            return None
+        try:
+            cp, _, _ = self._coefficients(hp)
+        except ValueError:
+            return None
+        pkey = (self._spec_token(), cp.tobytes())
+        hit = _prior_cache_get(pkey)
+        if hit is not None:
+            return hit
+        s = slot or self.slot()
+        dev = self.device
+        P, T = cp.shape
+        s.done.synchronize()
+        try:
+            with torch.cuda.device(dev):
+                coef_p = torch.from_numpy(np.ascontiguousarray(cp.ravel())).to(dev)
+                s.s_prior.wait_stream(torch.cuda.current_stream(dev))
+                with torch.cuda.stream(s.s_prior):
+                    self.assembly.assemble(s.ws_p, coef_p, s.s_prior)
+                    self._pobtaf(s.ws_p, False, s.scal[0:1], s.info[0:1], s.s_prior)
+                    s.host_scal.copy_(s.scal, non_blocking=True)
+                    s.host_info.copy_(s.info, non_blocking=True)
+                    s.done.record(s.s_prior)
+            s.done.synchronize()
+            val = (float(s.host_scal.numpy()[0]), int(s.host_info.numpy()[0]))
+        except Exception:
+            val = (float("nan"), -1)  # unblocks a deferred consumer, which then fails cleanly
+            _prior_cache_put(pkey, *val)
+            raise
+        _prior_cache_put(pkey, *val)
+        return val
+
+    def launch(self, theta, slot=None, defer_prior=False):
         """Issue one f_obj on the device without waiting.  Returns a handle
-        for :meth:`collect`, or None for a non-finite / invalid theta."""
+        for :meth:`collect`, or None for a non-finite / invalid theta.
+        ``defer_prior``: skip the prior factorization here; :meth:`collect`
+        takes log det Q_p from the shared cache (filled by
+        :meth:`prior_logdet` on another GPU)."""
         hp = self._hypers(theta)
         if not np.all(np.isfinite(hp.values)):
             return None
@@ -386,8 +440,11 @@ class ObjectiveEvaluator:
             # bits, one POBTAF fewer.
             pkey = (self._spec_token(), cp.tobytes()) if not same else None
             cached = _prior_cache_get(pkey) if pkey is not None else None
+            deferred = defer_prior and pkey is not None and cached is None
             with torch.cuda.stream(s.s_prior):
-                if cached is not None:
+                if deferred:
+                    pass  # log det Q_p arrives through the cache (prior_logdet elsewhere)
+                elif cached is not None:
                     s.scal[0:1].fill_(cached[0])
                     s.info[0:1].fill_(cached[1])
                 else:
@@ -413,20 +470,23 @@ class ObjectiveEvaluator:
                 s.host_scal.copy_(s.scal, non_blocking=True)
                 s.host_info.copy_(s.info, non_blocking=True)
                 s.done.record(s.s_cond)
-        return (s, hp, taus, same, pkey if cached is None else None)
+        return (s, hp, taus, same, pkey if cached is None else None, deferred)
 
     def collect(self, handle, want_mu=False):
         """Wait for a launched evaluation; returns (f, mu_perm_device or None)."""
         if handle is None:
             return -np.inf, None
-        s, hp, taus, same, pkey = handle
+        s, hp, taus, same, pkey, deferred = handle
         s.done.synchronize()
-        info = s.host_info.numpy()
-        if pkey is not None:
-            _prior_cache_put(pkey, float(s.host_scal.numpy()[0]), int(info[0]))
+        info = s.host_info.numpy().copy()
+        sc = s.host_scal.numpy().copy()
+        if deferred:
+            got = _prior_cache_wait(pkey)
+            sc[0], info[0] = got[0], (got[1] if np.isfinite(got[0]) else 1)
+        elif pkey is not None:
+            _prior_cache_put(pkey, float(sc[0]), int(info[0]))
         if info[0] != 0 or (not same and info[1] != 0):
             return -np.inf, None
-        sc = s.host_scal.numpy()
         ld_p = float(sc[0])
         ld_c = ld_p if same else float(sc[1])
         value = self.prior.log_density(hp.values)

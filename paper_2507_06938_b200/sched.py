@@ -143,11 +143,16 @@ class GpuRunner:
     ``depth`` at a time so several f_obj overlap on the device.
     """
 
-    def __init__(self, evaluators, negate=True, trace=None, depth=1):
+    def __init__(self, evaluators, negate=True, trace=None, depth=1, split_pairs=True):
         self.evaluators = list(evaluators)
         self.negate = negate
         self.trace = trace
         self.depth = max(1, int(depth))
+        # S2 across GPUs: a batch of at most G/2 points (the line search) runs
+        # each f_obj on a GPU pair -- Q_p's factorization on one, Q_c's chain
+        # on the other -- halving its latency; bigger batches (the gradient)
+        # run one f_obj per GPU.
+        self.split_pairs = bool(split_pairs) and len(self.evaluators) >= 2
         # one long-lived worker thread per GPU, always driving the same
         # evaluator: workspace slots are keyed by thread, so fresh (or
         # rotating) threads would allocate fresh Q_p / Q_c workspaces
@@ -155,8 +160,10 @@ class GpuRunner:
 
     @property
     def width(self):
-        """Evaluations that run concurrently (one per GPU)."""
-        return len(self.evaluators)
+        """Line-search candidates per round: one per GPU pair when f_obj is
+        split across a pair, else one per GPU."""
+        G = len(self.evaluators)
+        return G // 2 if self.split_pairs else G
 
     def close(self):
         for p in self._pools or []:
@@ -170,8 +177,44 @@ class GpuRunner:
             raise TypeError("GpuRunner needs fd_gradient-style tasks (lambda p=p: fun(p))")
         return np.asarray(d[0], dtype=np.float64)
 
+    def _pools_ready(self, G):
+        if self._pools is None:
+            self._pools = [ThreadPoolExecutor(max_workers=1) for _ in range(G)]
+
+    def _evaluate_split(self, points):
+        """Point k: prior half on GPU 2k (published through the shared prior
+        cache), conditional half on GPU 2k+1, which assembles f."""
+        G = len(self.evaluators)
+        sign = -1.0 if self.negate else 1.0
+        out = [None] * len(points)
+        self._pools_ready(G)
+
+        def prior(k):
+            self.evaluators[2 * k].prior_logdet(points[k])
+
+        def cond(k):
+            ev = self.evaluators[2 * k + 1]
+            out[k] = sign * ev.collect(ev.launch(points[k], defer_prior=True))[0]
+
+        futs = []
+        for k in range(len(points)):
+            futs.append(self._pools[2 * k].submit(prior, k))
+            futs.append(self._pools[2 * k + 1].submit(cond, k))
+        errors = []
+        for i, f in enumerate(futs):
+            try:
+                f.result()
+            except Exception as exc:  # report the lowest failing point
+                errors.append((i // 2, exc))
+        if errors:
+            idx, exc = min(errors, key=lambda p: p[0])
+            raise TaskError(idx, str(exc)) from exc
+        return out
+
     def evaluate_points(self, points):
         G = len(self.evaluators)
+        if self.split_pairs and 0 < len(points) <= G // 2:
+            return self._evaluate_split(points)
         sign = -1.0 if self.negate else 1.0
         out = [None] * len(points)
         failures = []
@@ -193,8 +236,7 @@ class GpuRunner:
         if G == 1:
             worker(0)
         else:
-            if self._pools is None:
-                self._pools = [ThreadPoolExecutor(max_workers=1) for _ in range(G)]
+            self._pools_ready(G)
             futs = [self._pools[g].submit(worker, g) for g in range(G)]
             for f in futs:
                 f.result()

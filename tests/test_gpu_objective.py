@@ -154,3 +154,30 @@ def test_prior_logdet_reuse_is_bitwise_and_skips_pobtaf(cuda):
     assert launches_cached < launches_fresh         # the prior assembly + POBTAF were skipped
     fr, _ = inla_np.evaluate(spec, moved, ev.prior.mean, ev.prior.sd)
     np.testing.assert_allclose(f_cached, fr, rtol=1e-10, atol=1e-10)
+
+
+def test_split_pair_evaluation_is_bitwise(cuda):
+    """S2 across a GPU pair (here two evaluators on one device): the prior half
+    on one, the conditional half on the other gives the same f bit for bit,
+    and a minimize driven by the split runner walks the serial path."""
+    inla = _inla()
+    from paper_2507_06938_b200 import sched
+
+    spec = make_spec(2, 3, 4, 1, 6, seed=11)
+    ev0 = inla.ObjectiveEvaluator(spec)
+    ev1 = inla.ObjectiveEvaluator(spec)
+    runner = sched.GpuRunner([ev0, ev1])
+    assert runner.split_pairs and runner.width == 1
+    theta = np.linspace(-0.1, 0.2, inla.HyperParams.dim_for(2))
+    inla.prior_cache_clear()
+    f_split = runner.evaluate_points([theta])[0]
+    inla.prior_cache_clear()
+    f_ref = -ev0.objective(theta)
+    assert f_split == f_ref
+    inla.prior_cache_clear()
+    serial = inla.minimize(ev0, np.zeros(theta.size), gtol=1e-4, ftol=1e-12, max_iter=15)
+    inla.prior_cache_clear()
+    par = inla.minimize(ev0, np.zeros(theta.size), gtol=1e-4, ftol=1e-12, max_iter=15, runner=runner)
+    assert par.theta.tolist() == serial.theta.tolist() and par.f == serial.f
+    assert par.iterations == serial.iterations
+    runner.close()
