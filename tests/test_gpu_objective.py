@@ -181,3 +181,30 @@ def test_split_pair_evaluation_is_bitwise(cuda):
     assert par.theta.tolist() == serial.theta.tolist() and par.f == serial.f
     assert par.iterations == serial.iterations
     runner.close()
+
+
+@pytest.mark.parametrize("name", ["ini", "biv"])
+def test_fit_matches_reference(cuda, name):
+    """Full pipeline (inla.py:661-729): mode within 1e-4, log posterior at the
+    mode within 1e-8 relative, the finite-difference Hessian at the mode
+    (1 + 2d + 2d(d-1) device f_obj) and the hyperparameter sds within 1e-5
+    relative, latent marginal means / sds within 1e-6 relative of the
+    unmodified reference's fit (tests/golden/fit.npz, oracle/make_golden_fit.py)."""
+    inla = _inla()
+    g = golden("fit.npz")
+    spec = spec_from_golden(g, f"{name}_")
+    gtol, ftol, gstep, hstep, psd = g[f"{name}_opts"]
+    opts = inla.FitOptions(grad_step=gstep, hess_step=hstep, gtol=gtol, ftol=ftol, prior_sd=psd)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        summary, res = inla.fit(spec, g[f"{name}_theta0"], opts)
+    assert summary.status == str(g[f"{name}_status"][0])
+    np.testing.assert_allclose(summary.theta_mode.values, g[f"{name}_theta"], atol=1e-4)
+    np.testing.assert_allclose(summary.logpost_at_mode, g[f"{name}_logpost"][0], rtol=1e-8)
+    h_ref = g[f"{name}_hessian"]
+    np.testing.assert_allclose(summary.theta_hessian, h_ref, rtol=1e-5,
+                               atol=1e-5 * np.abs(h_ref).max())
+    np.testing.assert_allclose(summary.theta_sd, g[f"{name}_theta_sd"], rtol=1e-5)
+    np.testing.assert_allclose(summary.latent_mean, g[f"{name}_latent_mean"], rtol=1e-6,
+                               atol=1e-6 * np.abs(g[f"{name}_latent_mean"]).max())
+    np.testing.assert_allclose(summary.latent_sd, g[f"{name}_latent_sd"], rtol=1e-6)
