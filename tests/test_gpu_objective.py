@@ -185,26 +185,44 @@ def test_split_pair_evaluation_is_bitwise(cuda):
 
 @pytest.mark.parametrize("name", ["ini", "biv"])
 def test_fit_matches_reference(cuda, name):
-    """Full pipeline (inla.py:661-729): mode within 1e-4, log posterior at the
-    mode within 1e-8 relative, the finite-difference Hessian at the mode
-    (1 + 2d + 2d(d-1) device f_obj) and the hyperparameter sds within 1e-5
-    relative, latent marginal means / sds within 1e-6 relative of the
-    unmodified reference's fit (tests/golden/fit.npz, oracle/make_golden_fit.py)."""
+    """Full pipeline (inla.py:661-729) against the unmodified reference's fit
+    (tests/golden/fit.npz, oracle/make_golden_fit.py).
+
+    Fit level: mode within 1e-4 (the north-star mode tolerance), log posterior
+    at the mode within 1e-8 relative.  The Hessian, the hyperparameter sds and
+    the latent marginals are functions of the mode, so at fit level they
+    inherit its 1e-4 tolerance (the inverse Hessian amplifies it: 2e-3 on the
+    sds).  Pointwise at the reference's own mode: the Hessian (1 + 2d + 2d(d-1)
+    device f_obj) within 1e-6 of its largest entry -- a second difference at
+    step 1e-2 scales the f_obj's ~1e-14 relative rounding by 1/h^2 = 1e4, and
+    the inverse then by cond(H), so the sds are held to 1e-3 relative -- and
+    the latent marginal means / sds to the FP64 1e-8 relative."""
     inla = _inla()
     g = golden("fit.npz")
     spec = spec_from_golden(g, f"{name}_")
     gtol, ftol, gstep, hstep, psd = g[f"{name}_opts"]
+    theta0 = g[f"{name}_theta0"]
     opts = inla.FitOptions(grad_step=gstep, hess_step=hstep, gtol=gtol, ftol=ftol, prior_sd=psd)
+    ev = inla.ObjectiveEvaluator(spec, prior=inla.ThetaPrior.for_dim(theta0.size, mean=theta0,
+                                                                      sd=psd))
     with warnings.catch_warnings():
         warnings.simplefilter("ignore")
-        summary, res = inla.fit(spec, g[f"{name}_theta0"], opts)
+        summary, res = inla.fit(ev, theta0, opts)
     assert summary.status == str(g[f"{name}_status"][0])
     np.testing.assert_allclose(summary.theta_mode.values, g[f"{name}_theta"], atol=1e-4)
     np.testing.assert_allclose(summary.logpost_at_mode, g[f"{name}_logpost"][0], rtol=1e-8)
     h_ref = g[f"{name}_hessian"]
-    np.testing.assert_allclose(summary.theta_hessian, h_ref, rtol=1e-5,
-                               atol=1e-5 * np.abs(h_ref).max())
-    np.testing.assert_allclose(summary.theta_sd, g[f"{name}_theta_sd"], rtol=1e-5)
-    np.testing.assert_allclose(summary.latent_mean, g[f"{name}_latent_mean"], rtol=1e-6,
-                               atol=1e-6 * np.abs(g[f"{name}_latent_mean"]).max())
-    np.testing.assert_allclose(summary.latent_sd, g[f"{name}_latent_sd"], rtol=1e-6)
+    np.testing.assert_allclose(summary.theta_hessian, h_ref, rtol=1e-3,
+                               atol=1e-3 * np.abs(h_ref).max())
+    np.testing.assert_allclose(summary.theta_sd, g[f"{name}_theta_sd"], rtol=2e-3)
+
+    # pointwise at the reference mode
+    t_ref = g[f"{name}_theta"]
+    hess = inla.fd_hessian(ev, t_ref, hstep)
+    np.testing.assert_allclose(hess, h_ref, rtol=1e-6, atol=1e-6 * np.abs(h_ref).max())
+    np.testing.assert_allclose(np.sqrt(np.diagonal(np.linalg.inv(hess))), g[f"{name}_theta_sd"],
+                               rtol=1e-3)
+    mean, sd = ev.latent_marginals(t_ref)
+    m_ref = g[f"{name}_latent_mean"]
+    np.testing.assert_allclose(mean, m_ref, rtol=1e-8, atol=1e-8 * np.abs(m_ref).max())
+    np.testing.assert_allclose(sd, g[f"{name}_latent_sd"], rtol=1e-8)
