@@ -228,6 +228,50 @@ def measure_c3(dev):
             "cpu_reference_f_obj_s_survey": 67.7}
 
 
+def measure_c3_iteration(n_gpus, max_iter=2):
+    """Measured north-star number at N GPUs: C3 L-BFGS iterations from theta0
+    (Armijo line search split over a GPU pair + the 31-point central-difference
+    gradient round-robin over the N GPUs, inla.py:535-605 / sched.py:99), one
+    ObjectiveEvaluator per GPU driven by sched.GpuRunner from this process."""
+    import warnings
+
+    import numpy as np
+    import torch
+
+    from paper_2507_06938_b200 import inla, sched
+    from paper_2507_06938_b200.synthetic import SyntheticSettings, generate_synthetic
+
+    th0 = np.array([-0.35, -0.25, -0.30, -0.20, -0.25, -0.25, 2.05, 2.05, 2.05, 0.05, 0.05,
+                    0.05, 0.65, -0.35, 0.35])
+    true = [-0.40, -0.30, -0.35, -0.25, -0.30, -0.30, 2.00, 2.00, 2.00, 0.00, 0.00, 0.00, 0.60,
+            -0.40, 0.30]
+    t0 = time.perf_counter()
+    data = generate_synthetic(SyntheticSettings(3, 1675, 48, 1, 80400), true, seed=2,
+                              device=torch.device("cuda", 0))
+    prior = inla.ThetaPrior.for_dim(15, mean=th0, sd=2.0)
+    evs = [inla.ObjectiveEvaluator(data.spec, prior=prior, device=torch.device("cuda", g))
+           for g in range(n_gpus)]
+    runner = sched.GpuRunner(evs)
+    runner.evaluate_points([th0] * n_gpus)  # warm every device
+    setup = time.perf_counter() - t0
+    inla.prior_cache_clear()
+    recs = []
+    t0 = time.perf_counter()
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        res = inla.minimize(evs[0], th0, gtol=1e-3, ftol=1e-12, max_iter=max_iter, runner=runner,
+                            on_iteration=recs.append)
+    total = time.perf_counter() - t0
+    for ev in evs:
+        ev.release_workspaces()
+    return {"model": "C3 trivariate n_v=3 n_s=1675 n_t=48 n_r=1 (b=5025, N=241203), "
+                     "L-BFGS from theta0",
+            "n_gpus": n_gpus, "iteration_s_measured": [r.seconds for r in recs],
+            "f_evals_per_iteration": [r.f_evals for r in recs],
+            "total_s_incl_first_gradient": total, "setup_s": setup, "f": res.f,
+            "timing": "host wall clock (perf_counter) around minimize; each f_obj synchronises"}
+
+
 # --------------------------------------------------------------- GPU leg
 def run_c5(args):
     """random SPD BTA (96*N, b, a), plan_partitions(96*N, N, lb),
@@ -445,6 +489,20 @@ def main():
     inla_obj = None
     if rank == 0 and world == 1 and not args.no_inla:
         inla_obj = measure_c3(dev)
+    if world > 1:
+        # every rank's timed work is done; the C3 north-star iteration then
+        # runs from rank 0 over all N GPUs of the run (ranks > 0 leave first)
+        dist.barrier()
+        dist.destroy_process_group()
+        if rank != 0:
+            return 0
+        if not args.no_inla:
+            del pristine, ws_f, ws_s, ws_i
+            torch.cuda.empty_cache()
+            try:
+                inla_obj = measure_c3_iteration(world)
+            except Exception as exc:  # the C2 line must still print
+                inla_obj = {"error": f"{type(exc).__name__}: {exc}"}
 
     if rank == 0:
         # roofline of the dominant routine (the longest launch chain of the step)
@@ -482,8 +540,6 @@ def main():
             "inla": inla_obj,
         }
         print(json.dumps(line), flush=True)
-    if world > 1:
-        dist.destroy_process_group()
     return 0
 
 
