@@ -288,6 +288,8 @@ def run_c5(args):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
+        # NCCL's version / debug lines default to stdout, which carries the JSON line
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
         dist.init_process_group("nccl", device_id=dev)
     n, b, a = 96 * world, args.b, args.a
     plan = bta_dist.plan_partitions(n, world, args.lb)
@@ -349,6 +351,8 @@ def main():
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
+        # NCCL's version / debug lines default to stdout, which carries the JSON line
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
         dist.init_process_group("nccl", device_id=dev)
     lib = _lib.load()
     n, b, a = args.n, args.b, args.a
