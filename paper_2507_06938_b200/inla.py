@@ -396,6 +396,21 @@ class ObjectiveEvaluator:
         _prior_cache_put(pkey, *val)
         return val
 
+    def prior_cached(self, theta):
+        """True when log det Q_p of ``theta`` is already in the shared prior
+        cache, i.e. an evaluation of it skips the prior POBTAF (about half
+        the cost of an f_obj).  Used by the runners to order work."""
+        if self.n_observations == 0:
+            return False
+        hp = self._hypers(theta)
+        if not np.all(np.isfinite(hp.values)):
+            return False
+        try:
+            cp, _, _ = self._coefficients(hp)
+        except ValueError:
+            return False
+        return _prior_cache_get((self._spec_token(), cp.tobytes())) is not None
+
     def launch(self, theta, slot=None, defer_prior=False):
         """Issue one f_obj on the device without waiting.  Returns a handle
         for :meth:`collect`, or None for a non-finite / invalid theta.

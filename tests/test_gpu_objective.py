@@ -226,3 +226,29 @@ def test_fit_matches_reference(cuda, name):
     m_ref = g[f"{name}_latent_mean"]
     np.testing.assert_allclose(mean, m_ref, rtol=1e-8, atol=1e-8 * np.abs(m_ref).max())
     np.testing.assert_allclose(sd, g[f"{name}_latent_sd"], rtol=1e-8)
+
+
+def test_gpu_runner_queue_orders_cached_points_last(cuda):
+    """Gradient batches (> G points) go through one cost-ordered queue: the
+    stencil points that only move the noise precisions find log det Q_p in
+    the prior cache (prior_cached) and run last; the gradient is the serial
+    one bit for bit."""
+    inla = _inla()
+    from paper_2507_06938_b200 import sched
+
+    nv = 2
+    spec = make_spec(nv, 3, 4, 1, 6, seed=21)
+    evs = [inla.ObjectiveEvaluator(spec) for _ in range(3)]
+    dim = inla.HyperParams.dim_for(nv)
+    theta = np.linspace(-0.15, 0.25, dim)
+    inla.prior_cache_clear()
+    f0, g0 = inla.fd_gradient(evs[0], theta)
+    inla.prior_cache_clear()
+    evs[0].objective(theta)
+    flags = [evs[0].prior_cached(theta + s * 1e-3 * e) for e in np.eye(dim) for s in (1, -1)]
+    assert any(flags) and not all(flags)
+    inla.prior_cache_clear()
+    runner = sched.GpuRunner(evs, split_pairs=False)
+    f1, g1 = inla.fd_gradient(evs[0], theta, runner=runner)
+    assert f0 == f1 and np.array_equal(g0, g1)
+    runner.close()
