@@ -288,8 +288,6 @@ def run_c5(args):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        # NCCL's version / debug lines default to stdout, which carries the JSON line
-        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
         dist.init_process_group("nccl", device_id=dev)
     n, b, a = 96 * world, args.b, args.a
     plan = bta_dist.plan_partitions(n, world, args.lb)
@@ -335,6 +333,12 @@ def run_c5(args):
 
 def main():
     args = parse_args()
+    # stdout carries exactly one JSON line: native libraries (NCCL's version
+    # banner, ...) write to fd 1, so fd 1 becomes stderr and Python's stdout
+    # keeps the original descriptor
+    out_fd = os.dup(1)
+    os.dup2(2, 1)
+    sys.stdout = os.fdopen(out_fd, "w", buffering=1)
     if args.impl == "reference":
         return run_reference(args)
     if args.config == "c5":
@@ -351,8 +355,6 @@ def main():
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        # NCCL's version / debug lines default to stdout, which carries the JSON line
-        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
         dist.init_process_group("nccl", device_id=dev)
     lib = _lib.load()
     n, b, a = args.n, args.b, args.a
