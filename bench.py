@@ -220,9 +220,10 @@ def measure_c3(dev):
             "f_obj_s": t, "f_obj_s_prior_cached": min(tc), "f_obj": f,
             "oracle_f_obj": -193110.15144130366,
             "iteration_s_est_8gpu": t * (1 + -(-31 // 8)),
-            # near the mode (1 line-search try, split over a GPU pair) + 31 gradient
-            # points round-robin over 8 GPUs (worst GPU: 4 full f_obj)
-            "iteration_s_est_8gpu_near_mode": max(min(tc), t / 2) + 4 * t,
+            # near the mode: 1 line-search try (split over a GPU pair) + the 30
+            # new gradient points through the cost-ordered queue on 8 GPUs (24
+            # full f_obj, 3 per GPU, then the 6 prior-cached ones)
+            "iteration_s_est_8gpu_near_mode": max(min(tc), t / 2) + 3 * t + min(tc),
             "iteration_s_est_1gpu": t * 32,
             "iteration_s_measured_4gpu": "12.0-13.2 (profiles/r01_c3_lbfgs_iterations_4gpu_v3.json)",
             "cpu_reference_f_obj_s_survey": 67.7}
