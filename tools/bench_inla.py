@@ -170,6 +170,38 @@ def c3fit(max_iter=60):
     }), flush=True)
 
 
+def c3post():
+    """C3 after the mode search (BASELINE configs[2]): the
+    finite-difference Hessian at the mode (1 + 2d + 2d(d-1) = 451 f_obj over
+    every visible GPU) and the latent marginals (POBTAS + POBTASI of Q_c)."""
+    G = torch.cuda.device_count()
+    data, prior = _c3_evaluator()
+    evs = [inla.ObjectiveEvaluator(data.spec, prior=prior, device=torch.device("cuda", g))
+           for g in range(G)]
+    runner = sched.GpuRunner(evs)
+    with open(os.path.join(os.path.dirname(__file__), "..", "profiles",
+                           "r01_c3_full_fit_4gpu.json")) as fh:
+        th = np.array(json.load(fh)["theta_star"])
+    runner.evaluate_points([th] * G)
+    inla.prior_cache_clear()
+    t0 = time.perf_counter()
+    hess = inla.fd_hessian(evs[0], th, 1e-2, runner)
+    t_h = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    mean, sd = evs[0].latent_marginals(th)
+    t_m = time.perf_counter() - t0
+    try:
+        np.linalg.cholesky(hess)
+        theta_sd = np.sqrt(np.diagonal(np.linalg.inv(hess))).tolist()
+    except np.linalg.LinAlgError:
+        theta_sd = None
+    print(json.dumps({
+        "config": f"C3 at the mode: fd_hessian (451 f_obj) over {G} GPUs + latent marginals",
+        "n_gpus": G, "hessian_s": t_h, "latent_marginals_s": t_m, "theta_sd": theta_sd,
+        "latent_sd_range": [float(sd.min()), float(sd.max())],
+    }), flush=True)
+
+
 if __name__ == "__main__":
     which = sys.argv[1] if len(sys.argv) > 1 else "c1"
     if which == "c1":
@@ -178,6 +210,8 @@ if __name__ == "__main__":
         c3()
     elif which == "c3fit":
         c3fit(int(sys.argv[2]) if len(sys.argv) > 2 else 60)
+    elif which == "c3post":
+        c3post()
     elif which == "c3iter":
         c3iter(int(sys.argv[2]) if len(sys.argv) > 2 else 2)
     else:
