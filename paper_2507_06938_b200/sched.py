@@ -6,8 +6,9 @@ lowest failing index re-raised.  The B200 build keeps that policy and adds two
 executors for the gradient layer (S1):
 
 * :class:`GpuRunner` — one process driving several GPUs of a box, one host
-  thread per GPU, task i -> GPU i % G, each GPU evaluating its share through
-  its own ObjectiveEvaluator (the device work releases the GIL).
+  thread per GPU, each GPU evaluating its share through its own
+  ObjectiveEvaluator (the device work releases the GIL); batches of at most G
+  points go task i -> GPU i % G, larger ones through a cost-ordered queue.
 * :class:`DistRunner` — one process per GPU (torchrun / NCCL): rank r evaluates
   tasks i with i % world == r, the scalar results are exchanged with one
   all-gather and every rank reassembles the identical list in index order,

@@ -314,3 +314,40 @@ def test_model_from_files_roundtrip(tmp_path):
         assert (got.design[i] != sp.csr_matrix(spec.design[i])).nnz == 0
         assert np.array_equal(got.observations[i], np.asarray(spec.observations[i]))
     assert got.joint_dim == spec.joint_dim
+
+
+def test_gpu_runner_queue_order_and_results_cpu():
+    """GpuRunner's gradient queue with stand-in evaluators (no GPU): results in
+    index order, the prior-cached points dispatched after every full one, the
+    lowest failing index re-raised."""
+    import threading
+
+    class FakeEv:
+        log, lock = [], threading.Lock()
+
+        def __init__(self, g):
+            self.g = g
+
+        def prior_cached(self, p):
+            return p[0] >= 10
+
+        def launch(self, p):
+            with FakeEv.lock:
+                FakeEv.log.append(int(p[0]))
+            if p[0] == 7 and getattr(FakeEv, "fail", False):
+                raise ValueError("boom")
+            return float(p[0])
+
+        def collect(self, h):
+            return (2.0 * h, None)
+
+    pts = [np.array([float(i)]) for i in range(14)]
+    runner = sched.GpuRunner([FakeEv(g) for g in range(3)], split_pairs=False)
+    out = runner.evaluate_points(pts)
+    assert out == [-2.0 * i for i in range(14)]
+    assert sorted(FakeEv.log[:10]) == list(range(10)) and sorted(FakeEv.log[10:]) == [10, 11, 12, 13]
+    FakeEv.fail = True
+    with pytest.raises(sched.TaskError) as ei:
+        runner.evaluate_points(pts)
+    assert ei.value.task_index == 7
+    runner.close()
