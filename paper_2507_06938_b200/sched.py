@@ -273,16 +273,15 @@ class GpuRunner:
             ev = self.evaluators[g]
             while True:
                 with lock:
-                    if nxt[0] >= len(order) or failures:
+                    if nxt[0] >= len(order):
                         return
                     i = order[nxt[0]]
                     nxt[0] += 1
                 try:
                     out[i] = sign * ev.collect(ev.launch(points[i]))[0]
-                except Exception as exc:
+                except Exception as exc:  # keep going: the lowest failing index is raised
                     with lock:
                         failures.append((i, exc))
-                    return
 
         self._pools_ready(G)
         futs = [self._pools[g].submit(worker, g) for g in range(G)]

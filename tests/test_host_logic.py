@@ -334,7 +334,7 @@ def test_gpu_runner_queue_order_and_results_cpu():
         def launch(self, p):
             with FakeEv.lock:
                 FakeEv.log.append(int(p[0]))
-            if p[0] == 7 and getattr(FakeEv, "fail", False):
+            if p[0] in (7, 12) and getattr(FakeEv, "fail", False):
                 raise ValueError("boom")
             return float(p[0])
 
