@@ -151,6 +151,29 @@ def prior_cache_clear():
         _PRIOR_ORDER.clear()
 
 
+# completed (non-aborted) factorizations of every evaluator of the process:
+# the numerator of the INLA-level useful TFLOP/s (bench.py)
+_WORK = {"pobtaf": 0, "pobtaf_flops": 0.0, "aborted": 0}
+_WORK_LOCK = threading.Lock()
+
+
+def work_counters():
+    """Snapshot of the completed-factorization counters."""
+    with _WORK_LOCK:
+        return dict(_WORK)
+
+
+def _count_pobtaf(n, b, a, arrow, ok):
+    from .perf import flops_pobtaf
+
+    with _WORK_LOCK:
+        if ok:
+            _WORK["pobtaf"] += 1
+            _WORK["pobtaf_flops"] += flops_pobtaf(n, b, a, arrow)
+        else:
+            _WORK["aborted"] += 1
+
+
 def _prior_cache_put(key, logdet, info):
     with _PRIOR_LOCK:
         if key in _PRIOR_CACHE:
@@ -389,6 +412,8 @@ class ObjectiveEvaluator:
                     s.done.record(s.s_prior)
             s.done.synchronize()
             val = (float(s.host_scal.numpy()[0]), int(s.host_info.numpy()[0]))
+            pm = self.pmap
+            _count_pobtaf(pm.n_blocks, pm.block_size, pm.arrow_size, False, val[1] == 0)
         except Exception:
             val = (float("nan"), -1)  # unblocks a deferred consumer, which then fails cleanly
             _prior_cache_put(pkey, *val)
@@ -500,6 +525,12 @@ class ObjectiveEvaluator:
             sc[0], info[0] = got[0], (got[1] if np.isfinite(got[0]) else 1)
         elif pkey is not None:
             _prior_cache_put(pkey, float(sc[0]), int(info[0]))
+        pm = self.pmap
+        if same or (pkey is not None and not deferred):
+            _count_pobtaf(pm.n_blocks, pm.block_size, pm.arrow_size, False, info[0] == 0)
+        if not same:
+            _count_pobtaf(pm.n_blocks, pm.block_size, pm.arrow_size,
+                          self.assembly.cond_has_arrow, info[1] == 0)
         if info[0] != 0 or (not same and info[1] != 0):
             return -np.inf, None
         ld_p = float(sc[0])
