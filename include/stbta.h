@@ -158,6 +158,24 @@ int stbta_residual(const long long* indptr, const int* indices, const double* va
                    long long nrows, const double* y, const double* x, const long long* seg,
                    int nseg, double* sq, double* out, void* stream);
 
+/* --------------------------------------------- time-partitioned solver --
+ * Coupling products of the partitioned solve (S3): the thin products that
+ * join a partition's interior solve to the reduced separator system
+ * (replaces the `@` / `np.einsum` couplings of bta_dist.d_solve,
+ * pkg/src/stinla/bta_dist.py:370-458):
+ *   Y_j += alpha * op(A_j) X_j, j < nbatch        (reduce == 0)
+ *   Y   += alpha * sum_j op(A_j) X_j, j ascending (reduce != 0)
+ * A_j: m x n row-major, row stride lda, batch stride strideA;
+ * op(A) = A (trans == 0: X_j n x k, Y_j m x k) or A^T (trans != 0: X_j m x k,
+ * Y_j n x k); X / Y rows are k wide with row strides ldx / ldy >= k and batch
+ * strides strideX / strideY (0 broadcasts X).  Fixed summation order
+ * (bitwise reproducible).  workspace >= stbta_couple_workspace_bytes(...). */
+size_t stbta_couple_workspace_bytes(int trans, int nbatch, int m, int n, int reduce);
+int stbta_couple(int trans, int nbatch, int m, int n, int k, double alpha, const double* A,
+                 long long lda, long long strideA, const double* X, long long ldx,
+                 long long strideX, double* Y, long long ldy, long long strideY, int reduce,
+                 void* workspace, size_t workspace_bytes, void* stream);
+
 /* ------------------------------------------------------------ dense GEMM --
  * C = alpha * op(A) * op(B) + beta * C on the FP64 DMMA engine (row-major,
  * op = transpose when ta/tb != 0).  Exposed for tests and benchmarks. */

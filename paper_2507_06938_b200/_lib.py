@@ -55,6 +55,12 @@ _SIGNATURES = {
         c_int,
         [c_int, c_int, c_int, c_int, c_int, c_dbl, c_vp, c_ll, c_vp, c_ll, c_dbl, c_vp, c_ll, c_vp],
     ),
+    "stbta_couple_workspace_bytes": (c_size, [c_int, c_int, c_int, c_int, c_int]),
+    "stbta_couple": (
+        c_int,
+        [c_int, c_int, c_int, c_int, c_int, c_dbl, c_vp, c_ll, c_ll, c_vp, c_ll, c_ll, c_vp, c_ll,
+         c_ll, c_int, c_vp, c_size, c_vp],
+    ),
     "stbta_stream_memops_supported": (c_int, []),
     "stbta_debug_globaltimer": (c_int, [c_vp, c_vp]),
     "stbta_upload_blocks": (c_int, [c_vp, c_vp, c_int, c_int, c_int, c_vp, ctypes.c_uint, c_vp]),

@@ -446,6 +446,14 @@ class AssemblyPlan:
                 cc[_pair_index(i, i), self.gram_col0 + i] = taus[i]
         return cp, cc
 
+    def rows_plan(self, t0, t1, with_tip, device):
+        """Assembly of block rows [t0, t1) only (one time partition, S3): the
+        entries whose storage slots fall in those rows (plus the tip when
+        ``with_tip``), re-addressed into a :class:`~.bta_dist.BTARows` flat
+        buffer ``diag (m,b,b) | lower (m,b,b) | arrow (m,a,b) [| tip (a,a)]``
+        with ``lower[j] = A(t0+j, t0+j-1)``; same basis table and coefficients."""
+        return _RowsAssembly(self, t0, t1, with_tip, device)
+
     def assemble_host(self, coef):
         """numpy evaluation of what :meth:`assemble` writes, in the flat
         reference layout (host checks)."""
@@ -495,3 +503,66 @@ class AssemblyPlan:
             ),
             "stbta_quadform",
         )
+
+
+class _RowsAssembly:
+    """Per-partition slice of an :class:`AssemblyPlan` (see ``rows_plan``)."""
+
+    def __init__(self, plan, t0, t1, with_tip, device):
+        pm = plan.pmap
+        n, b, a = pm.n_blocks, pm.block_size, pm.arrow_size
+        self.t0, self.t1, self.with_tip = t0, t1, with_tip
+        self.n, self.b, self.a = n, b, a
+        self.device = torch.device(device)
+        m, bb, ab = t1 - t0, b * b, a * b
+        e0 = n * bb
+        e1 = e0 + (n - 1) * bb
+        e2 = e1 + n * ab
+        off = plan.h_offsets
+        new = np.full(off.shape, -1, dtype=np.int64)
+        sel = (off >= t0 * bb) & (off < t1 * bb)  # diag rows
+        new[sel] = off[sel] - t0 * bb
+        lo_end = e0 + (t1 - 1) * bb  # lower blocks g = t-1 for rows t in [max(t0,1), t1)
+        lo_beg = e0 + (max(t0, 1) - 1) * bb
+        sel = (off >= lo_beg) & (off < lo_end)
+        new[sel] = m * bb + (off[sel] - e0) - (t0 - 1) * bb
+        sel = (off >= e1 + t0 * ab) & (off < e1 + t1 * ab)
+        new[sel] = 2 * m * bb + (off[sel] - e1 - t0 * ab)
+        if with_tip:
+            sel = off >= e2
+            new[sel] = 2 * m * bb + m * ab + (off[sel] - e2)
+        keep = new >= 0
+        self.nstore = 2 * m * bb + m * ab + (a * a if with_tip else 0)
+        order = np.argsort(new[keep], kind="stable")
+        offs = new[keep][order]
+        tile = _lib.ASM_TILE
+        ntiles = (self.nstore + tile - 1) // tile
+        starts = np.searchsorted(offs, np.arange(ntiles + 1, dtype=np.int64) * tile)
+        dev = self.device
+        self.n_terms = plan.n_terms
+        self.d_offsets = torch.from_numpy(offs).to(dev)
+        self.d_pair = torch.from_numpy(plan.h_pair[keep][order]).to(dev)
+        self.d_src = torch.from_numpy(plan.h_src[keep][order]).to(dev)
+        self.d_basis = plan.d_basis.to(dev)
+        self.d_starts = torch.from_numpy(starts.astype(np.int64)).to(dev)
+
+    def new_rows(self):
+        """A BTARows over a fresh flat buffer of this slice's layout."""
+        from .bta_dist import BTARows
+
+        buf = torch.empty(self.nstore, dtype=torch.float64, device=self.device)
+        return BTARows(self.n, self.t0, self.t1, self.b, self.a, self.device,
+                       with_tip=self.with_tip, data=buf)
+
+    def assemble(self, rows, coef_dev, stream=None):
+        """Zero-fill + scatter the slice's values into ``rows.data``."""
+        lib = _lib.load()
+        _lib.check(
+            lib.stbta_assemble(
+                _lib.ptr(rows.data), self.nstore, _lib.ptr(self.d_starts),
+                _lib.ptr(self.d_offsets), _lib.ptr(self.d_pair), _lib.ptr(self.d_src),
+                _lib.ptr(self.d_basis), _lib.ptr(coef_dev), self.n_terms,
+                _lib.stream_ptr(stream)),
+            "stbta_assemble",
+        )
+        return rows

@@ -214,7 +214,7 @@ class ObjectiveEvaluator:
     """
 
     def __init__(self, spec, prior=None, partitions=1, lb=1.0, pair_runner=None,
-                 calibrate_variance=False, device=None):
+                 calibrate_variance=False, device=None, devices=None):
         spec.validate()
         _lib.load()
         self.spec = spec
@@ -279,6 +279,12 @@ class ObjectiveEvaluator:
         self._npartial = 148 * 4
         self._slots = {}
         self._lock = threading.Lock()
+        # S3 (reference inla.py:287-308): with a multi-partition plan both
+        # factorizations of an f_obj run as PPOBTAF over time partitions, each
+        # assembled straight into its own block rows on devices[p % D]
+        self._dist = None
+        if self.plan is not None and self.plan.n_partitions > 1:
+            self._dist = _DistState(self, devices or [self.device])
 
     # -------------------------------------------------------------- helpers
 
@@ -396,6 +402,10 @@ class ObjectiveEvaluator:
         hit = _prior_cache_get(pkey)
         if hit is not None:
             return hit
+        if self._dist is not None:
+            val = self._dist.prior_logdet(cp)
+            _prior_cache_put(pkey, *val)
+            return val
         s = slot or self.slot()
         dev = self.device
         P, T = cp.shape
@@ -449,6 +459,8 @@ class ObjectiveEvaluator:
             cp, cc, taus = self._coefficients(hp)
         except ValueError:
             return None
+        if self._dist is not None:
+            return ("dist",) + self._dist.evaluate(hp, cp, cc, taus, defer_prior)
         s = slot or self.slot()
         dev = self.device
         P, T = cp.shape
@@ -516,6 +528,9 @@ class ObjectiveEvaluator:
         """Wait for a launched evaluation; returns (f, mu_perm_device or None)."""
         if handle is None:
             return -np.inf, None
+        if handle[0] == "dist":
+            value, mu = handle[1], handle[2]
+            return value, (mu if want_mu else None)
         s, hp, taus, same, pkey, deferred = handle
         s.done.synchronize()
         info = s.host_info.numpy().copy()
@@ -535,6 +550,18 @@ class ObjectiveEvaluator:
             return -np.inf, None
         ld_p = float(sc[0])
         ld_c = ld_p if same else float(sc[1])
+        value = self._combine(hp, taus, ld_p, ld_c, sc)
+        mu = None
+        if want_mu:
+            if self.n_observations:
+                mu = s.rhs.clone()
+            else:
+                mu = torch.zeros(self.spec.joint_dim, dtype=torch.float64, device=self.device)
+        return value, mu
+
+    def _combine(self, hp, taus, ld_p, ld_c, sc):
+        """f_obj from the log-dets and the device scalars [.., .., quad,
+        rss_0..rss_{nv-1}] (reference inla.py:360-371)."""
         value = self.prior.log_density(hp.values)
         if self.n_observations:
             active = taus > 0
@@ -548,13 +575,7 @@ class ObjectiveEvaluator:
             quad = 0.0
         value += 0.5 * ld_p - 0.5 * quad
         value -= 0.5 * ld_c
-        mu = None
-        if want_mu:
-            if self.n_observations:
-                mu = s.rhs.clone()
-            else:
-                mu = torch.zeros(self.spec.joint_dim, dtype=torch.float64, device=self.device)
-        return value, mu
+        return value
 
     def _pobtaf(self, buf, use_arrow, logdet_out, info_out, stream):
         """POBTAF on a (row-padded) scratch workspace."""
@@ -608,6 +629,8 @@ class ObjectiveEvaluator:
         POBTASI on the device (inla.py:376-395)."""
         hp = self._hypers(theta)
         cp, cc, taus = self._coefficients(hp)
+        if self._dist is not None:
+            return self._dist.latent_marginals(cc, taus)
         dev = self.device
         with torch.cuda.device(dev):
             ws = bta.BTAMatrix(self.pmap.n_blocks, self.pmap.block_size, self.pmap.arrow_size,
@@ -633,6 +656,126 @@ class ObjectiveEvaluator:
             if self.pmap.arrow_size:
                 var = torch.cat([var, torch.diagonal(inv.tip)])
             var = self.pmap.restore_vector(var.cpu().numpy())
+        return mu, np.sqrt(var)
+
+
+class _DistState:
+    """f_obj over time partitions (S3, reference inla.py:287-308 dispatching
+    to bta_dist): partition p's block rows of Q_p / Q_c are assembled on
+    devices[p % D] by a row-sliced assembly plan (no global workspace), its
+    interior eliminated there, the reduced system factorized on the
+    evaluator's device; the conditional mean comes from the partitioned
+    solve, the quadratic form and residuals from the same device kernels as
+    the one-GPU path."""
+
+    def __init__(self, ev, devices):
+        from . import bta_dist
+
+        self.ev = ev
+        self.bd = bta_dist
+        self.plan = ev.plan
+        self.devices = [torch.device(d) for d in devices]
+        P = self.plan.n_partitions
+        self.parts = [ev.assembly.rows_plan(self.plan.boundaries[p], self.plan.boundaries[p + 1],
+                                            p == 0, self.devices[p % len(self.devices)])
+                      for p in range(P)]
+        self.mapper = bta_dist._default_mapper(self.devices)
+        self.lock = threading.Lock()
+
+    def factorize(self, coef, use_arrow):
+        """PPOBTAF of the matrix with coefficient table ``coef``; raises
+        FactorizationError on a non-SPD pivot."""
+        pm = self.ev.pmap
+        n, b, a = pm.n_blocks, pm.block_size, pm.arrow_size
+        flat = np.ascontiguousarray(coef.ravel())
+        coefs = {}
+        for d in self.devices:
+            coefs.setdefault(str(d), torch.from_numpy(flat).to(d))
+        rows = [ra.assemble(ra.new_rows(), coefs[str(ra.device)]) for ra in self.parts]
+        chains = self.bd._make_chains(self.plan, b, a, use_arrow, self.devices)
+        tip = rows[0].tip.to(self.ev.device) if a else None
+        return self.bd._factorize_chains(self.plan, (n, b, a), chains,
+                                         lambda ch: ch.load(rows[ch.index]), tip, use_arrow,
+                                         self.ev.device, mapper=self.mapper)
+
+    def _logdet(self, coef, use_arrow):
+        pm = self.ev.pmap
+        try:
+            f = self.factorize(coef, use_arrow)
+        except bta.FactorizationError:
+            _count_pobtaf(pm.n_blocks, pm.block_size, pm.arrow_size, use_arrow, False)
+            return None, float("nan"), 1
+        _count_pobtaf(pm.n_blocks, pm.block_size, pm.arrow_size, use_arrow, True)
+        return f, self.bd.d_logdet(f), 0
+
+    def prior_logdet(self, cp):
+        with self.lock:
+            _, ld, info = self._logdet(cp, False)
+        return ld, info
+
+    def evaluate(self, hp, cp, cc, taus, defer_prior=False):
+        """(f, mu in BTA order on the evaluator's device or None)."""
+        ev = self.ev
+        lib = _lib.load()
+        same = ev.n_observations == 0
+        pkey = (ev._spec_token(), cp.tobytes()) if not same else None
+        with self.lock, torch.cuda.device(ev.device):
+            cached = _prior_cache_get(pkey) if pkey is not None else None
+            if cached is None and defer_prior and pkey is not None:
+                cached = _prior_cache_wait(pkey)
+            if cached is not None:
+                ld_p, info_p = cached[0], (cached[1] if np.isfinite(cached[0]) else 1)
+            else:
+                _, ld_p, info_p = self._logdet(cp, False)
+                if pkey is not None:
+                    _prior_cache_put(pkey, ld_p, info_p)
+            if info_p != 0:
+                return -np.inf, None
+            s = ev.slot()
+            s.scal.zero_()
+            if same:
+                ld_c = ld_p
+                mu = torch.zeros(ev.spec.joint_dim, dtype=torch.float64, device=ev.device)
+            else:
+                fc, ld_c, info_c = self._logdet(cc, ev.assembly.cond_has_arrow)
+                if info_c != 0:
+                    return -np.inf, None
+                coef = torch.from_numpy(np.concatenate([cp.ravel(), taus]).astype(np.float64)
+                                        ).to(ev.device)
+                coef_p, tau_d = coef[: cp.size], coef[cp.size :]
+                _lib.check(lib.stbta_rhs_combine(
+                    _lib.ptr(s.rhs), _lib.ptr(ev.d_U), _lib.ptr(tau_d), ev.n_processes,
+                    ev.spec.joint_dim, _lib.stream_ptr()), "rhs_combine")
+                mu = self.bd.d_solve(fc, s.rhs)
+                ev.assembly.quadform(coef_p, mu, s.partial, s.scal[2:3])
+                _lib.check(lib.stbta_residual(
+                    _lib.ptr(ev.d_indptr), _lib.ptr(ev.d_indices), _lib.ptr(ev.d_vals),
+                    ev.n_observations, _lib.ptr(ev.d_y), _lib.ptr(mu), _lib.ptr(ev.d_seg),
+                    ev.n_processes, _lib.ptr(s.sq), _lib.ptr(s.scal[3:]), _lib.stream_ptr()),
+                    "residual")
+            sc = s.scal.cpu().numpy()
+        return ev._combine(hp, taus, ld_p, ld_c, sc), mu
+
+    def latent_marginals(self, cc, taus):
+        """(mu, sd) via PPOBTAF + PPOBTAS + PPOBTASI of Q_c (inla.py:376-395)."""
+        ev = self.ev
+        dev = ev.device
+        with self.lock, torch.cuda.device(dev):
+            f = self.factorize(cc, ev.assembly.cond_has_arrow)
+            if ev.n_observations:
+                rhs = torch.empty(ev.spec.joint_dim, dtype=torch.float64, device=dev)
+                tau_d = torch.from_numpy(np.asarray(taus, dtype=np.float64)).to(dev)
+                _lib.check(_lib.load().stbta_rhs_combine(
+                    _lib.ptr(rhs), _lib.ptr(ev.d_U), _lib.ptr(tau_d), ev.n_processes,
+                    ev.spec.joint_dim, _lib.stream_ptr()), "rhs_combine")
+                mu = ev.pmap.restore_vector(self.bd.d_solve(f, rhs).cpu().numpy())
+            else:
+                mu = np.zeros(ev.spec.joint_dim)
+            inv = self.bd.d_selected_invert(f)
+            var = torch.diagonal(inv.diag, dim1=1, dim2=2).reshape(-1)
+            if ev.pmap.arrow_size:
+                var = torch.cat([var, torch.diagonal(inv.tip)])
+            var = ev.pmap.restore_vector(var.cpu().numpy())
         return mu, np.sqrt(var)
 
 
@@ -752,18 +895,25 @@ def _bfgs_inverse_update(hinv, delta, gamma):
 
 
 def minimize(objective, theta0, gtol=1e-3, ftol=1e-6, max_iter=100, grad_step=1e-3, runner=None,
-             c1=1e-4, shrink=0.5, max_backtracks=20, on_iteration=None):
+             c1=1e-4, shrink=0.5, max_backtracks=20, on_iteration=None, state0=None):
     """Quasi-Newton minimization with Armijo backtracking and central-difference
-    gradients — the reference algorithm (inla.py:504-613).  ``on_iteration``
-    (extension) is called with each IterationRecord."""
+    gradients — the reference algorithm (inla.py:504-613).  Extensions:
+    ``on_iteration`` is called with each IterationRecord; ``state0`` =
+    (f, grad, hinv) resumes a run at theta0 from a recorded BFGS state
+    (MinimizeResult.hinv) instead of the starting gradient and identity."""
     fun = _scalar_function(objective)
     theta = np.asarray(theta0, dtype=np.float64).copy()
     d = theta.size
-    f, grad = fd_gradient(fun, theta, grad_step, runner)
-    n_eval = 2 * d + 1
+    if state0 is None:
+        f, grad = fd_gradient(fun, theta, grad_step, runner)
+        n_eval = 2 * d + 1
+        hinv = np.eye(d)
+    else:
+        f, grad, hinv = float(state0[0]), np.array(state0[1], dtype=np.float64), \
+            np.array(state0[2], dtype=np.float64)
+        n_eval = 0
     if not np.isfinite(f):
         raise ValueError("objective is not finite at the starting point")
-    hinv = np.eye(d)
     trace = []
     status = "max_iterations"
     for it in range(1, max_iter + 1):
@@ -832,7 +982,9 @@ def minimize(objective, theta0, gtol=1e-3, ftol=1e-6, max_iter=100, grad_step=1e
             break
     if status == "max_iterations":
         warnings.warn("maximum iterations reached without convergence", stacklevel=2)
-    return MinimizeResult(theta, f, grad, len(trace), n_eval, status, trace)
+    res = MinimizeResult(theta, f, grad, len(trace), n_eval, status, trace)
+    res.hinv = hinv
+    return res
 
 
 def latent_marginals(theta, model):

@@ -87,3 +87,65 @@ def device_random_spd_bta(n, b, a, seed=0, device="cuda"):
             tip += fac_a[i] @ fac_a[i].T
         T.copy_(tip)
     return data
+
+
+@torch.no_grad()
+def device_random_spd_rows(n, b, a, t0, t1, seed=0, device="cuda", with_tip=True):
+    """Block rows [t0, t1) of an SPD BTA matrix L L^T of the reference
+    generator's law (bta.py:362-394), drawn in HBM by the rank that owns them:
+    every factor block of L is drawn from its own generator seeded by (seed,
+    block, kind), so any rank can produce its rows without the rest of the
+    matrix (the partitioned benchmark).  Rows t need the
+    factor blocks of t and t-1.  The tip (sum over ALL arrow factor blocks)
+    is built when ``with_tip`` (the root)."""
+    from .bta_dist import BTARows
+
+    dev = torch.device(device)
+    sd = 0.3 / b**0.5
+    f64 = torch.float64
+
+    def gen(i, kind):
+        g = torch.Generator(device=dev)
+        g.manual_seed(int(seed) * 1_000_003 + 4 * i + kind)
+        return g
+
+    def ld(i):  # lower factor of diagonal block i
+        g = gen(i, 0)
+        x = torch.tril(torch.randn(b, b, dtype=f64, device=dev, generator=g) * sd, -1)
+        x.diagonal().copy_(1.0 + torch.rand(b, dtype=f64, device=dev, generator=g))
+        return x
+
+    def ls(i):  # factor block (i, i-1), i >= 1
+        return torch.randn(b, b, dtype=f64, device=dev, generator=gen(i, 1)) * sd
+
+    def la(i):  # arrow factor block of column block i
+        return torch.randn(a, b, dtype=f64, device=dev, generator=gen(i, 2)) * sd
+
+    rows = BTARows(n, t0, t1, b, a, dev, with_tip=with_tip)
+    prev_d = ld(t0 - 1) if t0 > 0 else None
+    prev_a = la(t0 - 1) if t0 > 0 and a else None
+    for t in range(t0, t1):
+        d = ld(t)
+        rows.d(t).copy_(d @ d.T)
+        if a:
+            at = la(t)
+            rows.arw(t).copy_(at @ d.T)
+        if t > 0:
+            s = ls(t)
+            rows.d(t).add_(s @ s.T)
+            rows.low(t).copy_(s @ prev_d.T)
+            if a:
+                rows.arw(t).add_(prev_a @ s.T)
+        prev_d = d
+        if a:
+            prev_a = at
+    if with_tip and a:
+        g = gen(n, 3)
+        ft = torch.tril(torch.randn(a, a, dtype=f64, device=dev, generator=g) * sd, -1)
+        ft.diagonal().copy_(1.0 + torch.rand(a, dtype=f64, device=dev, generator=g))
+        tip = ft @ ft.T
+        for i in range(n):
+            x = la(i)
+            tip += x @ x.T
+        rows.tip.copy_(tip)
+    return rows

@@ -95,7 +95,12 @@ def test_dist_multi_device(cuda):
     n, b, a = 16, 130, 3
     data = bta_np.random_spd_bta(rng, n, b, a)
     ref = data.copy()
-    bta_np.factorize(ref, n, b, a)
+    has = bta_np.factorize(ref, n, b, a)
     f = bta_dist.d_factorize(bta.BTAMatrix(n, b, a, data), bta_dist.plan_partitions(n, 4),
                              devices=[0, 1])
     np.testing.assert_allclose(bta_dist.d_logdet(f), bta_np.logdet(ref, n, b, a), rtol=1e-9)
+    rhs = rng.normal(size=(n * b + a, 2))
+    np.testing.assert_allclose(bta_dist.d_solve(f, rhs), bta_np.solve(ref, n, b, a, has, rhs),
+                               rtol=1e-9, atol=1e-10)
+    np.testing.assert_allclose(bta_dist.d_selected_invert(f).numpy(),
+                               bta_np.selected_invert(ref, n, b, a, has), rtol=1e-8, atol=1e-11)

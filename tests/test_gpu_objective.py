@@ -252,3 +252,32 @@ def test_gpu_runner_queue_orders_cached_points_last(cuda):
     f1, g1 = inla.fd_gradient(evs[0], theta, runner=runner)
     assert f0 == f1 and np.array_equal(g0, g1)
     runner.close()
+
+
+@pytest.mark.parametrize("nv,parts,lb", [(1, 2, 1.0), (2, 3, 1.6), (3, 2, 1.0), (1, 4, 1.0)])
+def test_partitioned_objective_matches_sequential(cuda, nv, parts, lb):
+    """f_obj through S3 (reference inla.py:287-308: d_factorize / d_logdet /
+    d_solve for both precision matrices) equals the one-chain evaluator:
+    f and mu to 1e-10, latent marginal variances to 1e-10."""
+    import torch
+
+    inla = _inla()
+    spec = make_spec(nv, 5, 9, 1, 12, seed=70 + nv)
+    ev = inla.ObjectiveEvaluator(spec)
+    G = torch.cuda.device_count()
+    devices = [torch.device("cuda", g % G) for g in range(2)]
+    evp = inla.ObjectiveEvaluator(spec, partitions=parts, lb=lb, devices=devices)
+    assert evp.plan.n_partitions == parts
+    rng = np.random.default_rng(3 + nv)
+    for _ in range(3):
+        theta = rng.normal(scale=0.3, size=inla.HyperParams.dim_for(nv))
+        inla.prior_cache_clear()
+        f, mu = ev.evaluate(theta)
+        inla.prior_cache_clear()
+        fp, mup = evp.evaluate(theta)
+        np.testing.assert_allclose(fp, f, rtol=1e-10)
+        np.testing.assert_allclose(mup, mu, rtol=1e-10, atol=1e-12)
+    m1, s1 = ev.latent_marginals(theta)
+    m2, s2 = evp.latent_marginals(theta)
+    np.testing.assert_allclose(m2, m1, rtol=1e-10, atol=1e-12)
+    np.testing.assert_allclose(s2 ** 2, s1 ** 2, rtol=1e-10)
