@@ -114,8 +114,6 @@ int stbta_pobtasi_ex(const double* Ld, const double* Ll, const double* La, const
  *     on copy_stream, each gated on the recursion's completion counter of that
  *     block; record an event on copy_stream to know when host_out is final. */
 int stbta_stream_memops_supported(void);
-/* Debug: *out (device u64) = %globaltimer (ns) when this point of `stream` runs. */
-int stbta_debug_globaltimer(unsigned long long* out, void* stream);
 int stbta_upload_blocks(double* dst, const double* src_host, int n, int b, int a, unsigned* ready,
                         unsigned epoch, void* stream);
 int stbta_pobtaf_ready(double* data, int n, int b, int a, int use_arrow, double* logdet_out,
@@ -176,13 +174,6 @@ int stbta_couple(int trans, int nbatch, int m, int n, int k, double alpha, const
                  long long strideX, double* Y, long long ldy, long long strideY, int reduce,
                  void* workspace, size_t workspace_bytes, void* stream);
 
-/* ------------------------------------------------------------ dense GEMM --
- * C = alpha * op(A) * op(B) + beta * C on the FP64 DMMA engine (row-major,
- * op = transpose when ta/tb != 0).  Exposed for tests and benchmarks. */
-int stbta_dgemm(int ta, int tb, int M, int N, int K, double alpha, const double* A, long long lda,
-                const double* B, long long ldb, double beta, double* C, long long ldc,
-                void* stream);
-
 /* ------------------------------------------------------- instrumentation --
  * Kernel launches issued by this library since load (host counter; bench.py
  * reports the difference over its timed region as gpu_launches). */
@@ -194,21 +185,9 @@ long long stbta_launch_count(void);
  * kind (POTRF, TRSM, UPDATE, STRIP), {count, ns waiting, ns executing};
  * NULL disables (the default). */
 void stbta_debug_set_profile(unsigned long long* buf);
-/* Debug micro-benchmark: `grid` CTAs each run `reps` tile products
- * C_t -= A_t B_t^T (128x128, depth K) of CTA shape `variant`. */
-int stbta_debug_tile_bench(int variant, const double* A, const double* B, double* C, int ntile,
-                           int reps, int grid, int K, void* stream);
-/* Debug micro-benchmark: `grid` CTAs each factorize + invert the SPD 128x128
- * tile A `reps` times; ph (6 u64) receives CTA 0's phase times in ns. */
-int stbta_debug_potrf_bench(const double* A, double* out, int reps, int grid,
-                            unsigned long long* ph, void* stream);
-/* Debug: clock cycles of `iters` dependent DMMA (which=0) or DFMA (1) on one warp. */
-int stbta_debug_latency(int which, int iters, double* scratch, long long* cycles, void* stream);
-/* Debug: DMMA throughput with shared-memory fragment loads (mode 0 LDS.64,
- * 1 LDS.128, 2 none); FLOPs = grid*8*iters*8*32*512. */
-int stbta_debug_lds_bench(int mode, int iters, int grid, double* out, void* stream);
+/* Launch blocks x 256 threads, each warp issuing iters*16 DMMA.8x8x4:
+ * FLOPs = blocks*8*iters*16*512. */
 int stbta_probe_dmma(int blocks, int iters, double* scratch, void* stream);
-int stbta_probe_dfma(int blocks, int iters, double* scratch, void* stream);
 
 #ifdef __cplusplus
 }

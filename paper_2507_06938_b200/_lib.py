@@ -12,6 +12,7 @@ import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libstbta.so")
+TOOLS_LIB_PATH = os.path.join(_HERE, "libstbta_tools.so")
 
 _lib = None
 
@@ -51,10 +52,6 @@ _SIGNATURES = {
     ),
     "stbta_pobtasi_workspace_bytes": (c_size, [c_int, c_int, c_int]),
     "stbta_pobtasi": (c_int, [c_vp, c_vp, c_int, c_int, c_int, c_int, c_vp, c_size, c_vp]),
-    "stbta_dgemm": (
-        c_int,
-        [c_int, c_int, c_int, c_int, c_int, c_dbl, c_vp, c_ll, c_vp, c_ll, c_dbl, c_vp, c_ll, c_vp],
-    ),
     "stbta_couple_workspace_bytes": (c_size, [c_int, c_int, c_int, c_int, c_int]),
     "stbta_couple": (
         c_int,
@@ -62,7 +59,6 @@ _SIGNATURES = {
          c_ll, c_int, c_vp, c_size, c_vp],
     ),
     "stbta_stream_memops_supported": (c_int, []),
-    "stbta_debug_globaltimer": (c_int, [c_vp, c_vp]),
     "stbta_upload_blocks": (c_int, [c_vp, c_vp, c_int, c_int, c_int, c_vp, ctypes.c_uint, c_vp]),
     "stbta_pobtaf_ready": (
         c_int,
@@ -74,12 +70,7 @@ _SIGNATURES = {
     ),
     "stbta_launch_count": (c_ll, []),
     "stbta_debug_set_profile": (None, [c_vp]),
-    "stbta_debug_potrf_bench": (c_int, [c_vp, c_vp, c_int, c_int, c_vp, c_vp]),
-    "stbta_debug_lds_bench": (c_int, [c_int, c_int, c_int, c_vp, c_vp]),
-    "stbta_debug_latency": (c_int, [c_int, c_int, c_vp, c_vp, c_vp]),
-    "stbta_debug_tile_bench": (c_int, [c_int, c_vp, c_vp, c_vp, c_int, c_int, c_int, c_int, c_vp]),
     "stbta_probe_dmma": (c_int, [c_int, c_int, c_vp, c_vp]),
-    "stbta_probe_dfma": (c_int, [c_int, c_int, c_vp, c_vp]),
     "stbta_assemble_tile_elems": (c_int, []),
     "stbta_assemble": (c_int, [c_vp, c_ll, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_int, c_vp]),
     "stbta_quadform": (
@@ -88,6 +79,20 @@ _SIGNATURES = {
     ),
     "stbta_rhs_combine": (c_int, [c_vp, c_vp, c_vp, c_int, c_ll, c_vp]),
     "stbta_residual": (c_int, [c_vp, c_vp, c_vp, c_ll, c_vp, c_vp, c_vp, c_int, c_vp, c_vp, c_vp]),
+}
+
+# tools-only library (include/stbta_tools.h): micro-benchmarks, debug probes
+_TOOLS_SIGNATURES = {
+    "stbta_dgemm": (
+        c_int,
+        [c_int, c_int, c_int, c_int, c_int, c_dbl, c_vp, c_ll, c_vp, c_ll, c_dbl, c_vp, c_ll, c_vp],
+    ),
+    "stbta_debug_globaltimer": (c_int, [c_vp, c_vp]),
+    "stbta_debug_potrf_bench": (c_int, [c_vp, c_vp, c_int, c_int, c_vp, c_vp]),
+    "stbta_debug_lds_bench": (c_int, [c_int, c_int, c_int, c_vp, c_vp]),
+    "stbta_debug_latency": (c_int, [c_int, c_int, c_vp, c_vp, c_vp]),
+    "stbta_debug_tile_bench": (c_int, [c_int, c_vp, c_vp, c_vp, c_int, c_int, c_int, c_int, c_vp]),
+    "stbta_probe_dfma": (c_int, [c_int, c_int, c_vp, c_vp]),
 }
 
 
@@ -119,6 +124,23 @@ def load(require_cuda=True):
     if require_cuda and not torch.cuda.is_available():
         raise StbtaError("stbta needs a CUDA device (sm_100a); no CPU fallback exists")
     return lib
+
+
+_tools = None
+
+
+def load_tools():
+    """The tools-only library (micro-benchmarks / debug probes for tools/)."""
+    global _tools
+    if _tools is None:
+        load()
+        lib = ctypes.CDLL(TOOLS_LIB_PATH)
+        for name, (res, args) in _TOOLS_SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _tools = lib
+    return _tools
 
 
 def exported_symbols():

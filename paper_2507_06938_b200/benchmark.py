@@ -4,7 +4,8 @@ Mirrors the reference CLI's ``benchmark`` command (pkg/src/stinla/cli.py:174-266
 SURVEY.md §8(f) f4): for every load-balance factor and partition count it runs
 ``d_factorize`` of a random SPD BTA matrix and of its prior-like copy (arrow
 zeroed, identity tip), ``d_solve`` and ``d_selected_invert``, and writes
-``benchmark.csv`` with the reference schema
+``benchmark.csv`` (plus the evaluation-layer ``task_trace.csv``,
+cli.py:243-256) with the reference schema
 
     routine,P,lb,n,b,a,phase,seconds,flop_count
 
@@ -25,7 +26,7 @@ import os
 import numpy as np
 import torch
 
-from . import bta, bta_dist
+from . import bta, bta_dist, sched
 from .bta import OpCounter
 from .inla import load_balance_ratio
 
@@ -48,9 +49,10 @@ def write_table(path, header, rows):
 
 
 def run_benchmark(n=32, b=4, a=4, partitions=(1, 2, 3, 4), lb_values=(1.0, 1.6), seed=1,
-                  out_dir="."):
+                  out_dir=".", workers=1):
     """Rows of the reference benchmark table (cli.py:186-229) measured on the
-    device path; writes ``out_dir/benchmark.csv`` and returns the rows."""
+    device path; writes ``out_dir/benchmark.csv`` and the evaluation-layer
+    ``task_trace.csv`` (cli.py:243-256) and returns the rows."""
     rng = np.random.default_rng(seed)
     matrix = bta.random_spd_bta(rng, n, b, a)
     prior_like = matrix.copy()
@@ -92,6 +94,15 @@ def run_benchmark(n=32, b=4, a=4, partitions=(1, 2, 3, 4), lb_values=(1.0, 1.6),
     os.makedirs(out_dir, exist_ok=True)
     write_table(os.path.join(out_dir, "benchmark.csv"), HEADER,
                 [[r[k] for k in HEADER] for r in rows])
+
+    # evaluation-layer trace (cli.py:243-256): one gradient-sized batch of 31
+    # factorization tasks dealt over the worker pool, task i -> group i % g1
+    small = bta.random_spd_bta(rng, max(2, n // 4), b, a)
+    tasks = [(lambda m=small.copy(): bta.logdet(bta.factorize(m))) for _ in range(31)]
+    trace = []
+    sched.run_tasks(tasks, sched.allocate(workers, dim_theta=15), trace=trace)
+    write_table(os.path.join(out_dir, "task_trace.csv"), ["task", "group", "round", "start", "stop"],
+                [(r.index, r.group, r.round, r.start, r.stop) for r in trace])
     return rows
 
 
@@ -104,16 +115,19 @@ def main(argv=None):
     ap.add_argument("--partitions", default="1,2,3,4")
     ap.add_argument("--lb", default="1.0,1.6")
     ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--workers", type=int, default=1)
     args = ap.parse_args(argv)
     rows = run_benchmark(args.n, args.b, args.a,
                          tuple(int(v) for v in args.partitions.split(",")),
-                         tuple(float(v) for v in args.lb.split(",")), args.seed, args.out)
+                         tuple(float(v) for v in args.lb.split(",")), args.seed, args.out,
+                         args.workers)
     bta_flops = max(r["flop_count"] for r in rows if r["routine"] == "factorize" and r["P"] == 1)
     bt_flops = max(r["flop_count"] for r in rows if r["routine"] == "factorize_bt" and r["P"] == 1)
     print(f"benchmark: n={args.n} b={args.b} a={args.a}; factorization work ratio "
           f"{bta_flops / bt_flops:.4f} (asymptotic model "
           f"{1 + load_balance_ratio(args.b, args.a):.4f})")
-    print(f"outputs: {os.path.join(args.out, 'benchmark.csv')}")
+    print(f"outputs: {os.path.join(args.out, 'benchmark.csv')}, "
+          f"{os.path.join(args.out, 'task_trace.csv')}")
     return 0
 
 

@@ -30,7 +30,6 @@
 #include "../../include/stbta.h"
 #include "band.cuh"
 #include "potrf_tile.cuh"
-#include "stbta_internal.cuh"
 #include "tile_mma.cuh"
 #include "tma_mma.cuh"
 #include "memops.cuh"
@@ -874,21 +873,3 @@ static int pobtaf_impl(double* diag, double* lower, double* arrow, double* tip, 
   }
   return 0;
 }
-
-extern "C" {
-
-int stbta_dgemm(int ta, int tb, int M, int N, int K, double alpha, const double* A, long long lda,
-                const double* B, long long ldb, double beta, double* C, long long ldc,
-                void* stream) {
-  if (M < 0 || N < 0 || K < 0) return STBTA_EARG;
-  GemmArgs gm{};
-  gm.A = seg1(const_cast<double*>(A), lda);
-  gm.B = seg1(const_cast<double*>(B), ldb);
-  gm.C = seg1(C, ldc);
-  gm.M = M; gm.N = N; gm.K = K;
-  gm.alpha = alpha; gm.beta = beta;
-  gm.batch = 1;
-  return gemm_launch(gm, ta != 0, tb != 0, reinterpret_cast<cudaStream_t>(stream));
-}
-
-}  // extern "C"

@@ -23,7 +23,6 @@
 #include "../../include/stbta.h"
 #include "band.cuh"
 #include "potrf_tile.cuh"
-#include "stbta_internal.cuh"
 #include "tile_mma.cuh"
 #include "tma_mma.cuh"
 #include "memops.cuh"

@@ -1,7 +1,8 @@
-// FP64 tensor-pipe peak probe: a register-resident DMMA.8x8x4 loop with
-// enough independent accumulators to saturate the pipe.  Used by bench.py to
-// measure the FP64 roofline denominator on the box (MEASURED_PEAKS.json has
-// no FP64 entry).
+// Library runtime: the launch counter (bench.py's gpu_launches), the
+// optional POBTAF profile hook, the stream-ordered zero fill, and the FP64
+// tensor-pipe peak probe -- a register-resident DMMA.8x8x4 loop with enough
+// independent accumulators to saturate the pipe, bench.py's roofline
+// denominator (MEASURED_PEAKS.json has no FP64 entry).
 #include "../../include/stbta.h"
 #include "common.cuh"
 
@@ -30,61 +31,12 @@ __global__ void __launch_bounds__(256) dmma_probe_kernel(int iters, double* out)
   if (s == 12345.678) out[0] = s;  // keep the loop alive
 }
 
-__global__ void __launch_bounds__(256) dfma_probe_kernel(int iters, double* out) {
-  constexpr int ACC = 8;
-  double c[ACC];
-  const double a = 1.0 + threadIdx.x * 1e-9, b = 1.0 - threadIdx.x * 1e-12;
-#pragma unroll
-  for (int i = 0; i < ACC; ++i) c[i] = i;
-  for (int it = 0; it < iters; ++it) {
-#pragma unroll
-    for (int i = 0; i < ACC; ++i) c[i] = fma(c[i], a, b);
-  }
-  double s = 0.0;
-#pragma unroll
-  for (int i = 0; i < ACC; ++i) s += c[i];
-  if (s == 12345.678) out[0] = s;
-}
-
-// Dependent-chain latency probes: one warp, `iters` dependent DMMA / DFMA.
-__global__ void dmma_latency_kernel(int iters, double* out, long long* cycles) {
-  double c0 = 0.0, c1 = 0.0;
-  const double a = 1.0 + threadIdx.x * 1e-9, b = 1.0 - threadIdx.x * 1e-9;
-  const long long t0 = clock64();
-  for (int it = 0; it < iters; ++it) dmma884(c0, c1, a, b);
-  const long long t1 = clock64();
-  if (threadIdx.x == 0) cycles[0] = t1 - t0;
-  if (c0 + c1 == 12345.678) out[0] = c0;
-}
-__global__ void dfma_latency_kernel(int iters, double* out, long long* cycles) {
-  double c = threadIdx.x;
-  const double a = 1.0 + threadIdx.x * 1e-9, b = 1.0 - threadIdx.x * 1e-12;
-  const long long t0 = clock64();
-  for (int it = 0; it < iters; ++it) c = fma(c, a, b);
-  const long long t1 = clock64();
-  if (threadIdx.x == 0) cycles[0] = t1 - t0;
-  if (c == 12345.678) out[0] = c;
-}
-
 }  // namespace stbta
 
 extern "C" {
-int stbta_debug_latency(int which, int iters, double* scratch, long long* cycles, void* stream) {
-  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  if (which == 0) stbta::dmma_latency_kernel<<<1, 32, 0, st>>>(iters, scratch, cycles);
-  else stbta::dfma_latency_kernel<<<1, 32, 0, st>>>(iters, scratch, cycles);
-  return (int)cudaGetLastError();
-}
-
 long long stbta_launch_count(void) { return stbta::g_launches.load(); }
 // Debug hook: see include/stbta.h.
 void stbta_debug_set_profile(unsigned long long* buf) { stbta::g_prof = buf; }
-// blocks x 256 threads, each thread iters*8 DFMA.  FLOPs = blocks*256*iters*16.
-int stbta_probe_dfma(int blocks, int iters, double* scratch, void* stream) {
-  stbta::dfma_probe_kernel<<<blocks, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(iters,
-                                                                                        scratch);
-  return (int)cudaGetLastError();
-}
 // Launch blocks x 256 threads, each warp issuing iters*16 DMMA.8x8x4
 // (256 FMA each).  FLOPs = blocks * 8 * iters * 16 * 512.
 int stbta_probe_dmma(int blocks, int iters, double* scratch, void* stream) {
@@ -124,15 +76,3 @@ int zero_async(void* p, size_t bytes, cudaStream_t st) {
 
 }  // namespace stbta
 
-namespace stbta {
-__global__ void globaltimer_kernel(unsigned long long* out) {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  *out = t;
-}
-}  // namespace stbta
-
-extern "C" int stbta_debug_globaltimer(unsigned long long* out, void* stream) {
-  stbta::globaltimer_kernel<<<1, 1, 0, reinterpret_cast<cudaStream_t>(stream)>>>(out);
-  return (int)cudaGetLastError();
-}

@@ -9,6 +9,7 @@
 // wavefronts per 256-byte warp load).
 #include <cstdio>
 
+#include "../../../include/stbta_tools.h"
 #include "gemm.cuh"
 
 namespace stbta {
@@ -230,3 +231,18 @@ int gemm_launch(const GemmArgs& g, bool ta, bool tb, cudaStream_t stream) {
 }
 
 }  // namespace stbta
+
+extern "C" int stbta_dgemm(int ta, int tb, int M, int N, int K, double alpha, const double* A,
+                           long long lda, const double* B, long long ldb, double beta, double* C,
+                           long long ldc, void* stream) {
+  using namespace stbta;
+  if (M < 0 || N < 0 || K < 0) return STBTA_EARG;
+  GemmArgs gm{};
+  gm.A = seg1(const_cast<double*>(A), lda);
+  gm.B = seg1(const_cast<double*>(B), ldb);
+  gm.C = seg1(C, ldc);
+  gm.M = M; gm.N = N; gm.K = K;
+  gm.alpha = alpha; gm.beta = beta;
+  gm.batch = 1;
+  return gemm_launch(gm, ta != 0, tb != 0, reinterpret_cast<cudaStream_t>(stream));
+}

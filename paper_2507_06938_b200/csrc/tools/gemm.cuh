@@ -13,7 +13,7 @@
 // and its arrowhead rows; C may have a third region for the tip.
 #pragma once
 
-#include "common.cuh"
+#include "../common.cuh"
 
 namespace stbta {
 

@@ -1,8 +1,8 @@
 // Micro-benchmarks of the task-graph building blocks (debug exports, not part
 // of the solver path): the UPDATE tile product in isolation, per CTA shape.
-#include "../../include/stbta.h"
-#include "potrf_tile.cuh"
-#include "tile_mma.cuh"
+#include "../../../include/stbta_tools.h"
+#include "../potrf_tile.cuh"
+#include "../tile_mma.cuh"
 
 namespace stbta {
 

@@ -402,15 +402,14 @@ class ObjectiveEvaluator:
         hit = _prior_cache_get(pkey)
         if hit is not None:
             return hit
-        if self._dist is not None:
-            val = self._dist.prior_logdet(cp)
-            _prior_cache_put(pkey, *val)
-            return val
-        s = slot or self.slot()
         dev = self.device
-        P, T = cp.shape
-        s.done.synchronize()
         try:
+            if self._dist is not None:
+                val = self._dist.prior_logdet(cp)
+                _prior_cache_put(pkey, *val)
+                return val
+            s = slot or self.slot()
+            s.done.synchronize()
             with torch.cuda.device(dev):
                 coef_p = torch.from_numpy(np.ascontiguousarray(cp.ravel())).to(dev)
                 s.s_prior.wait_stream(torch.cuda.current_stream(dev))
@@ -785,13 +784,22 @@ def eval_objective(theta, model):
 
 
 def _scalar_function(objective):
+    """Callables pass through; evaluators and model specs become the negated
+    objective (inla.py:405-415).  The closure is tagged with its evaluator so
+    the GPU runners can re-bind a task to an identical evaluator on another
+    device (sched.GpuRunner); untagged tasks are simply called."""
     if callable(objective) and not isinstance(objective, ObjectiveEvaluator):
         return objective
     if hasattr(objective, "objective"):  # an evaluator (or evaluator-like object)
         ev = objective
     else:  # a model spec
         ev = ObjectiveEvaluator(objective)
-    return lambda theta: -ev.objective(theta)
+
+    def neg_objective(theta):
+        return -ev.objective(theta)
+
+    neg_objective.stbta_evaluator = ev
+    return neg_objective
 
 
 def _stencil(theta, step, cross):
@@ -818,7 +826,13 @@ def _stencil(theta, step, cross):
 
 
 def _run(fun, points, runner):
-    tasks = [lambda p=p: fun(p) for p in points]
+    tasks = []
+    for p in points:
+        def task(p=p):
+            return fun(p)
+
+        task.stbta_point, task.stbta_fun = p, fun  # lets a GPU runner re-bind the task
+        tasks.append(task)
     if runner is None:
         return np.asarray([t() for t in tasks])
     return np.asarray(runner(tasks))

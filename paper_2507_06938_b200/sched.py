@@ -139,10 +139,15 @@ class GpuRunner:
     evaluator of GPU (i % G) and run by one host thread per GPU.
 
     ``evaluators[g]`` is an ObjectiveEvaluator on GPU g.  The runner is called
-    by :func:`inla.fd_gradient` with closures ``lambda p=p: fun(p)``; it
-    recovers each point ``p`` and evaluates ``-evaluators[g].objective(p)``
-    (the minimized function of the reference).  Per GPU the tasks are issued
-    ``depth`` at a time so several f_obj overlap on the device.
+    by :func:`inla.fd_gradient` / ``minimize`` / ``fd_hessian`` with tasks
+    tagged with their point and function (``inla._run``).  When the function
+    is the negated objective of an evaluator equivalent to the runner's (same
+    model spec, prior and variance calibration -- every f_obj is then the same
+    bits on any of them), each point is re-bound to the evaluator of GPU
+    (i % G) and ``-evaluators[g].objective(p)`` is evaluated there; any other
+    task is simply called, one thread per GPU, so a user callable is never
+    replaced.  Per GPU the tasks are issued ``depth`` at a time so several
+    f_obj overlap on the device.
     """
 
     def __init__(self, evaluators, negate=True, trace=None, depth=1, split_pairs=True):
@@ -159,6 +164,7 @@ class GpuRunner:
         # evaluator: workspace slots are keyed by thread, so fresh (or
         # rotating) threads would allocate fresh Q_p / Q_c workspaces
         self._pools = None
+        self.dispatch_log = None  # list: queue dispatch order (tests)
 
     @property
     def width(self):
@@ -172,12 +178,32 @@ class GpuRunner:
             p.shutdown(wait=True)
         self._pools = None
 
-    @staticmethod
-    def _point(task):
-        d = task.__defaults__
-        if not d:
-            raise TypeError("GpuRunner needs fd_gradient-style tasks (lambda p=p: fun(p))")
-        return np.asarray(d[0], dtype=np.float64)
+    def _compatible(self, ev):
+        """Does evaluator ``ev`` compute the same f_obj as the runner's?"""
+        if any(ev is e for e in self.evaluators):
+            return True
+        ref = self.evaluators[0]
+        try:
+            return (ev.spec is ref.spec
+                    and np.array_equal(ev.prior.mean, ref.prior.mean)
+                    and np.array_equal(ev.prior.sd, ref.prior.sd)
+                    and np.array_equal(ev.calibration, ref.calibration))
+        except AttributeError:
+            return False
+
+    def _points(self, tasks):
+        """The tasks' points when every task is a tagged negated objective of
+        an equivalent evaluator (and the runner negates), else None."""
+        if not self.negate:
+            return None
+        pts = []
+        for t in tasks:
+            p = getattr(t, "stbta_point", None)
+            ev = getattr(getattr(t, "stbta_fun", None), "stbta_evaluator", None)
+            if p is None or ev is None or not self._compatible(ev):
+                return None
+            pts.append(np.asarray(p, dtype=np.float64))
+        return pts
 
     def _pools_ready(self, G):
         if self._pools is None:
@@ -230,12 +256,19 @@ class GpuRunner:
             for k in range(0, len(mine), self.depth):
                 batch = mine[k : k + self.depth]
                 slots = [ev.slot(j) for j in range(len(batch))] if self.depth > 1 else [None]
-                try:
-                    handles = [ev.launch(points[i], slot=s) for i, s in zip(batch, slots)]
-                    for i, h in zip(batch, handles):
+                handles = []
+                for i, s in zip(batch, slots):
+                    try:
+                        handles.append((i, ev.launch(points[i], slot=s)))
+                    except Exception as exc:  # the index that actually failed
+                        failures.append((i, exc))
+                        break
+                for i, h in handles:
+                    try:
                         out[i] = sign * ev.collect(h)[0]
-                except Exception as exc:
-                    failures.append((batch[0], exc))
+                    except Exception as exc:
+                        failures.append((i, exc))
+                if failures:
                     return
 
         if G == 1:
@@ -277,6 +310,8 @@ class GpuRunner:
                         return
                     i = order[nxt[0]]
                     nxt[0] += 1
+                    if self.dispatch_log is not None:
+                        self.dispatch_log.append(i)
                 try:
                     out[i] = sign * ev.collect(ev.launch(points[i]))[0]
                 except Exception as exc:  # keep going: the lowest failing index is raised
@@ -293,7 +328,12 @@ class GpuRunner:
         return out
 
     def __call__(self, tasks):
-        return self.evaluate_points([self._point(t) for t in tasks])
+        tasks = list(tasks)
+        pts = self._points(tasks)
+        if pts is not None:
+            return self.evaluate_points(pts)
+        G = len(self.evaluators)
+        return run_tasks(tasks, LayerAllocation(workers=G, g1=G, g2=1, g3=1))
 
 
 class DistRunner:
@@ -314,25 +354,45 @@ class DistRunner:
     def width(self):
         return self.world
 
-    def evaluate_points(self, points):
+    def _run_mine(self, n, call):
+        """Run this rank's indices (i % world == rank) through call(i); values
+        and failure flags are all-gathered, results returned in index order
+        on every rank, and a failure anywhere raises the same TaskError (the
+        lowest failing index) on every rank."""
         import torch
 
-        sign = -1.0 if self.negate else 1.0
-        n = len(points)
-        mine = list(range(self.rank, n, self.world))
-        local = torch.full((n,), float("nan"), dtype=torch.float64)
-        for i in mine:
-            local[i] = sign * self.evaluator.objective(points[i])
+        local = torch.full((2, n), float("nan"), dtype=torch.float64)
+        local[1].zero_()
+        errors = {}
+        for i in range(self.rank, n, self.world):
+            try:
+                local[0, i] = call(i)
+            except Exception as exc:  # published, raised below on every rank
+                local[1, i] = 1.0
+                errors[i] = exc
         backend = self.dist.get_backend(self.group)
         dev = self.evaluator.device if backend == "nccl" else torch.device("cpu")
         buf = local.to(dev)
         gathered = [torch.empty_like(buf) for _ in range(self.world)]
         self.dist.all_gather(gathered, buf, group=self.group)
-        out = np.empty(n)
+        out, failed = np.empty(n), np.zeros(n, dtype=bool)
         for r in range(self.world):
-            vals = gathered[r].cpu().numpy()
-            out[r::self.world] = vals[r::self.world]
+            g = gathered[r].cpu().numpy()
+            out[r::self.world] = g[0, r::self.world]
+            failed[r::self.world] = g[1, r::self.world] != 0
+        if failed.any():
+            idx = int(np.flatnonzero(failed)[0])
+            exc = errors.get(idx)
+            raise TaskError(idx, str(exc) if exc else "failed on another rank") from exc
         return out.tolist()
 
+    def evaluate_points(self, points):
+        sign = -1.0 if self.negate else 1.0
+        return self._run_mine(len(points),
+                              lambda i: sign * self.evaluator.objective(points[i]))
+
     def __call__(self, tasks):
-        return self.evaluate_points([GpuRunner._point(t) for t in tasks])
+        """Each rank calls its own tasks (i % world == rank): every task is a
+        deterministic function of its point, so no re-binding is needed."""
+        tasks = list(tasks)
+        return self._run_mine(len(tasks), lambda i: float(tasks[i]()))

@@ -47,7 +47,19 @@ def _worker(rank, world, port, out):
         pts = [np.full(4, 0.1 * k) for k in range(9)]
         vals = runner.evaluate_points(pts)
         res = inla.minimize(ev, np.zeros(4), gtol=1e-8, ftol=1e-14, max_iter=50, runner=runner)
-        out[rank] = (vals, res.theta.tolist(), res.f, res.iterations)
+        # a failing task raises the same (lowest) index on every rank
+        def bad(k):
+            def t():
+                if k in (3, 6):
+                    raise ValueError("boom")
+                return float(k)
+            return t
+        try:
+            runner([bad(k) for k in range(8)])
+            err = None
+        except sched.TaskError as e:
+            err = e.task_index
+        out[rank] = (vals, res.theta.tolist(), res.f, res.iterations, err)
     finally:
         dist.destroy_process_group()
 
@@ -63,7 +75,8 @@ def test_dist_runner_gloo_world2():
     serial_vals = [-ev.objective(np.full(4, 0.1 * k)) for k in range(9)]
     serial = inla.minimize(ev, np.zeros(4), gtol=1e-8, ftol=1e-14, max_iter=50)
     for r in range(2):
-        vals, theta, f, its = out[r]
+        vals, theta, f, its, err = out[r]
+        assert err == 3
         assert vals == serial_vals  # index order, minimized sign, bitwise
         assert theta == serial.theta.tolist() and f == serial.f and its == serial.iterations
     np.testing.assert_allclose(out[0][1], np.linalg.solve(ev.h, ev.h @ ev.c), atol=1e-6)

@@ -28,3 +28,12 @@ def test_benchmark_table_matches_reference_rows(cuda, tmp_path):
     assert table[0] == benchmark.HEADER
     assert len(table) == 1 + len(gold["rows"])
     assert all(float(r[7]) > 0 for r in table[1:])  # seconds
+    # evaluation-layer trace (reference cli.py:243-256): 31 tasks dealt i -> i % g1
+    rows = benchmark.run_benchmark(c["n"], c["b"], c["a"], (1,), (1.0,), c["seed"],
+                                   str(tmp_path), workers=4)
+    with open(tmp_path / "task_trace.csv") as fh:
+        trace = list(csv.reader(fh))
+    assert trace[0] == ["task", "group", "round", "start", "stop"]
+    assert [int(r[0]) for r in trace[1:]] == list(range(31))
+    assert [int(r[1]) for r in trace[1:]] == [i % 4 for i in range(31)]
+    assert [int(r[2]) for r in trace[1:]] == [i // 4 for i in range(31)]

@@ -121,8 +121,8 @@ def test_allocation_golden():
     assert a.g3 >= 2
 
 
-def _header_symbols():
-    txt = open(os.path.join(ROOT, "include", "stbta.h")).read()
+def _header_symbols(name="stbta.h"):
+    txt = open(os.path.join(ROOT, "include", name)).read()
     txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
     return sorted(set(re.findall(r"\b(stbta_[a-z0-9_]+)\s*\(", txt)))
 
@@ -136,6 +136,12 @@ def test_cabi_library_exports_every_header_symbol():
     from paper_2507_06938_b200 import _lib
 
     assert set(_lib.exported_symbols()) >= set(syms)
+    # the tools-only library (micro-benchmarks / debug probes) is separate
+    tools = ctypes.CDLL(os.path.join(ROOT, "paper_2507_06938_b200", "libstbta_tools.so"))
+    for s in _header_symbols("stbta_tools.h"):
+        if s not in syms:
+            assert hasattr(tools, s), s
+            assert s not in _lib.exported_symbols(), s
     # pure-host entry points callable without a GPU
     lib.stbta_storage_elems.restype = ctypes.c_longlong
     assert lib.stbta_storage_elems(48, 5025, 3) == 2399532984
@@ -343,11 +349,56 @@ def test_gpu_runner_queue_order_and_results_cpu():
 
     pts = [np.array([float(i)]) for i in range(14)]
     runner = sched.GpuRunner([FakeEv(g) for g in range(3)], split_pairs=False)
+    runner.dispatch_log = []  # recorded inside the dispatch critical section
     out = runner.evaluate_points(pts)
     assert out == [-2.0 * i for i in range(14)]
-    assert sorted(FakeEv.log[:10]) == list(range(10)) and sorted(FakeEv.log[10:]) == [10, 11, 12, 13]
+    log = runner.dispatch_log
+    assert log[:10] == list(range(10)) and log[10:] == [10, 11, 12, 13]
+    runner.dispatch_log = None
     FakeEv.fail = True
     with pytest.raises(sched.TaskError) as ei:
         runner.evaluate_points(pts)
     assert ei.value.task_index == 7
+    runner.close()
+
+
+def test_gpu_runner_calls_untagged_and_foreign_tasks():
+    """GpuRunner re-binds only tagged negated objectives of an equivalent
+    evaluator; user callables and other evaluators' objectives are called
+    as given (the reference runner contract: execute these tasks)."""
+    from paper_2507_06938_b200 import inla
+
+    class Ev:
+        def __init__(self, scale, spec):
+            self.scale, self.spec = scale, spec
+            self.prior = inla.ThetaPrior.for_dim(2)
+            self.calibration = np.zeros(1)
+
+        def objective(self, p):
+            return self.scale * float(np.sum(p))
+
+        def launch(self, p):
+            return self.objective(p)
+
+        def collect(self, h):
+            return (h, None)
+
+        def prior_cached(self, p):
+            return False
+
+    spec = object()
+    runner = sched.GpuRunner([Ev(1.0, spec), Ev(1.0, spec)], split_pairs=False)
+    # user callable: called as is
+    f = lambda p: 10.0 * float(np.sum(p))  # noqa: E731
+    _, g = inla.fd_gradient(f, np.array([0.5, 1.0]), 1e-3, runner=runner)
+    np.testing.assert_allclose(g, [10.0, 10.0])
+    # an evaluator of another model: its own objective, not the runner's
+    other = Ev(3.0, object())
+    _, g = inla.fd_gradient(other, np.array([0.5, 1.0]), 1e-3, runner=runner)
+    np.testing.assert_allclose(g, [-3.0, -3.0])
+    # an equivalent evaluator (same spec / prior / calibration): re-bound to
+    # the runner's evaluators (the stand-in's scale only shows which one ran)
+    twin = Ev(5.0, spec)
+    _, g = inla.fd_gradient(twin, np.array([0.5, 1.0]), 1e-3, runner=runner)
+    np.testing.assert_allclose(g, [-1.0, -1.0])
     runner.close()

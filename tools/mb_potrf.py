@@ -3,7 +3,7 @@ import sys, os
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from paper_2507_06938_b200 import _lib
-lib = _lib.load(); dev = torch.device("cuda"); st = _lib.stream_ptr()
+lib = _lib.load_tools(); dev = torch.device("cuda"); st = _lib.stream_ptr()
 X = torch.randn(128, 128, dtype=torch.float64, device=dev) * 0.05
 A = (X @ X.T + torch.eye(128, dtype=torch.float64, device=dev) * 2).contiguous()
 out = torch.zeros(4, dtype=torch.float64, device=dev)

@@ -3,7 +3,7 @@ import sys, os
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from paper_2507_06938_b200 import _lib
-lib = _lib.load(); dev = torch.device("cuda"); st = _lib.stream_ptr()
+lib = _lib.load_tools(); dev = torch.device("cuda"); st = _lib.stream_ptr()
 ntile = 148
 for K in (128, 256, 1024):
     A = torch.randn(ntile, 128, K, dtype=torch.float64, device=dev)

@@ -3,9 +3,9 @@ import sys, os, subprocess, time, statistics
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from paper_2507_06938_b200 import _lib
-lib = _lib.load(); dev = torch.device("cuda"); st = _lib.stream_ptr()
+lib = _lib.load_tools(); dev = torch.device("cuda"); st = _lib.stream_ptr()
 sc = torch.zeros(16, dtype=torch.float64, device=dev)
-for name, fn, fl in (("dmma", lib.stbta_probe_dmma, lambda b, it: b * 8 * it * 16 * 512),
+for name, fn, fl in (("dmma", _lib.load().stbta_probe_dmma, lambda b, it: b * 8 * it * 16 * 512),
                      ("dfma", lib.stbta_probe_dfma, lambda b, it: b * 256 * it * 16)):
     blocks, iters = 148 * 4, 20000
     fn(blocks, 100, _lib.ptr(sc), st); torch.cuda.synchronize()
