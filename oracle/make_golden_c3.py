@@ -1,13 +1,19 @@
 """Golden vectors for the north-star model itself:
 trivariate coregional n_v=3, n_s=1675, n_t=48, n_r=1, 80 400 observations per
 process, seed 2, theta0 / theta_true of pkg/configs/trivariate.ini:14-15, prior
-N(theta0, 2^2) (trivariate.ini:16).  Generated by the UNMODIFIED reference
-(stinla) on the host cores of the development container: one evaluate at
-theta0 (f_obj and the conditional mean) and the 31-point central-difference
-gradient batch of fd_gradient (inla.py:418-437), every task value kept.
-Test infrastructure only (about 40 min, 20 GB RSS):
+N(theta0, 2^2) (trivariate.ini:16).  Everything is computed by the UNMODIFIED
+reference (stinla): its generate_synthetic (once, in the parent), then one
+evaluate at theta0 (f_obj and the conditional mean) and the 31-point
+central-difference gradient batch of fd_gradient (inla.py:418-437), every
+task value kept.  Test infrastructure only.
 
-    PYTHONDONTWRITEBYTECODE=1 python oracle/make_golden_c3.py
+A C3 f_obj costs the reference 6-20 minutes of CPU, so the 32 evaluations
+run in parallel worker processes (the f_obj of a point does not depend on
+where it runs; the task values are reduced exactly as fd_gradient does).
+The reference is taken from $STINLA_REF (default /root/reference/pkg/src;
+on the GPU box's 32-core host: baseline/_ref, the pip-installed copy):
+
+    PYTHONDONTWRITEBYTECODE=1 python oracle/make_golden_c3.py [workers] [threads]
 
 Output: tests/golden/c3.npz (no model inputs -- they are 10^5-sized; the
 tests rebuild them with the package's generator and check the stored input
@@ -15,17 +21,21 @@ checksums first).
 """
 
 import os
+import pickle
 import sys
+import tempfile
 import time
 
 import numpy as np
 
-from make_golden import OUT, REF
+OUT = os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "tests", "golden")
+REF = os.environ.get("STINLA_REF", "/root/reference/pkg/src")
 
 THETA0 = np.array([-0.35, -0.25, -0.30, -0.20, -0.25, -0.25, 2.05, 2.05, 2.05, 0.05, 0.05,
                    0.05, 0.65, -0.35, 0.35])
 THETA_TRUE = np.array([-0.40, -0.30, -0.35, -0.25, -0.30, -0.30, 2.00, 2.00, 2.00, 0.00, 0.00,
                        0.00, 0.60, -0.40, 0.30])
+STEP = 1e-3
 # latent entries sampled for the mean check (joint variable-major indices)
 MU_SAMPLE = np.unique(np.concatenate([np.arange(0, 241203, 997), [241200, 241201, 241202]]))
 
@@ -41,48 +51,77 @@ def input_checksums(spec):
     return np.array(out)
 
 
-def main():
+def _points():
+    """fd_gradient's task order (inla.py:428-436): centre, then +h / -h per
+    coordinate."""
+    pts = [THETA0.copy()]
+    for i in range(THETA0.size):
+        for sign in (1.0, -1.0):
+            p = THETA0.copy()
+            p[i] += sign * STEP
+            pts.append(p)
+    return pts
+
+
+def _worker(args):
+    spec_path, k, threads = args
+    os.environ["OPENBLAS_NUM_THREADS"] = str(threads)
     sys.path.insert(0, REF)
-    from stinla.inla import ObjectiveEvaluator, ThetaPrior, fd_gradient
+    from threadpoolctl import threadpool_limits
+
+    from stinla.inla import ObjectiveEvaluator, ThetaPrior
+
+    with open(spec_path, "rb") as fh:
+        spec = pickle.load(fh)
+    with threadpool_limits(threads):
+        ev = ObjectiveEvaluator(spec, prior=ThetaPrior.for_dim(15, mean=THETA0, sd=2.0))
+        t0 = time.perf_counter()
+        if k == 0:
+            f, mu = ev.evaluate(THETA0)
+            return k, f, mu[MU_SAMPLE], float(mu.sum()), time.perf_counter() - t0
+        # the gradient's task k-1: the minimized (negated) objective
+        f = -ev.objective(_points()[k - 1])
+        return k, f, None, None, time.perf_counter() - t0
+
+
+def main():
+    import multiprocessing as mp
+
+    workers = int(sys.argv[1]) if len(sys.argv) > 1 else 2
+    threads = int(sys.argv[2]) if len(sys.argv) > 2 else max(1, (os.cpu_count() or 2) // workers)
+    sys.path.insert(0, REF)
     from stinla.synthetic import SyntheticSettings, generate_synthetic
 
     t0 = time.perf_counter()
     data = generate_synthetic(SyntheticSettings(3, 1675, 48, 1, 80400), THETA_TRUE, seed=2)
     t_gen = time.perf_counter() - t0
-    prior = ThetaPrior.for_dim(15, mean=THETA0, sd=2.0)
+    print(f"reference generate_synthetic: {t_gen:.1f} s", flush=True)
+    tmp = tempfile.NamedTemporaryFile(suffix=".pkl", delete=False)
+    pickle.dump(data.spec, tmp)
+    tmp.close()
+    jobs = [(tmp.name, k, threads) for k in range(32)]
+    res = {}
     t0 = time.perf_counter()
-    ev = ObjectiveEvaluator(data.spec, prior=prior)
-    t_init = time.perf_counter() - t0
-    t0 = time.perf_counter()
-    f0, mu = ev.evaluate(THETA0)
-    t_f = time.perf_counter() - t0
-    print(f"f_obj(theta0) = {f0!r} in {t_f:.1f} s (gen {t_gen:.1f} s, init {t_init:.1f} s)",
-          flush=True)
-    vals = []
-
-    def runner(tasks):
-        out = []
-        for k, t in enumerate(tasks):
-            tic = time.perf_counter()
-            out.append(t())
-            print(f"  task {k}: {out[-1]!r} ({time.perf_counter() - tic:.1f} s)", flush=True)
-        vals.extend(out)
-        return out
-
-    t0 = time.perf_counter()
-    fneg, grad = fd_gradient(ev, THETA0, 1e-3, runner=runner)
-    t_g = time.perf_counter() - t0
+    with mp.get_context("spawn").Pool(workers) as pool:
+        for k, f, mu, mus, secs in pool.imap_unordered(_worker, jobs):
+            res[k] = (f, mu, mus, secs)
+            print(f"  job {k}: {f!r} ({secs:.1f} s)", flush=True)
+    os.unlink(tmp.name)
+    vals = np.array([res[k][0] for k in range(1, 32)])
+    grad = (vals[1::2] - vals[2::2]) / (2.0 * STEP)  # inla.py:436
+    f0, mu, mus, _ = res[0]
     np.savez_compressed(
         os.path.join(OUT, "c3.npz"),
         theta0=THETA0, theta_true=THETA_TRUE, prior_sd=np.array([2.0]),
         settings=np.array([3, 1675, 48, 1, 80400, 2]),
         input_checksums=input_checksums(data.spec),
-        f_obj=np.array([f0]), mu_index=MU_SAMPLE, mu=mu[MU_SAMPLE], mu_sum=np.array([mu.sum()]),
-        grad_step=np.array([1e-3]), task_values=np.array(vals), neg_f=np.array([fneg]),
-        grad=grad,
-        seconds=np.array([t_gen, t_init, t_f, t_g]),
+        f_obj=np.array([f0]), mu_index=MU_SAMPLE, mu=mu, mu_sum=np.array([mus]),
+        grad_step=np.array([STEP]), task_values=vals, neg_f=np.array([vals[0]]), grad=grad,
+        seconds=np.array([t_gen, time.perf_counter() - t0]),
+        task_seconds=np.array([res[k][3] for k in range(32)]),
+        threads=np.array([workers, threads]),
     )
-    print(f"gradient batch {t_g:.1f} s; c3 golden written", flush=True)
+    print(f"c3 golden written: f_obj {f0!r}, |grad|_inf {np.abs(grad).max():.6g}", flush=True)
 
 
 if __name__ == "__main__":

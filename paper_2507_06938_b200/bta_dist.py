@@ -920,8 +920,10 @@ def _gather_flat(local, sizes, root, group):
     dist = _dist()
     rank = dist.get_rank(group)
     if rank != root:
-        dist.send(local.contiguous(), dist.get_global_rank(group, root) if group else root,
-                  group=group)
+        op = dist.P2POp(dist.isend, local.contiguous(),
+                        dist.get_global_rank(group, root) if group else root, group=group)
+        for req in dist.batch_isend_irecv([op]):
+            req.wait()
         return None
     out, ops = [], []
     for r, size in enumerate(sizes):
@@ -944,7 +946,10 @@ def _scatter_flat(parts, size, root, group, device):
     rank = dist.get_rank(group)
     if rank != root:
         buf = torch.empty(size, dtype=torch.float64, device=device)
-        dist.recv(buf, dist.get_global_rank(group, root) if group else root, group=group)
+        op = dist.P2POp(dist.irecv, buf, dist.get_global_rank(group, root) if group else root,
+                        group=group)
+        for req in dist.batch_isend_irecv([op]):
+            req.wait()
         return buf
     ops = []
     for r, part in enumerate(parts):
