@@ -13,7 +13,17 @@ where it runs; the task values are reduced exactly as fd_gradient does).
 The reference is taken from $STINLA_REF (default /root/reference/pkg/src;
 on the GPU box's 32-core host: baseline/_ref, the pip-installed copy):
 
-    PYTHONDONTWRITEBYTECODE=1 python oracle/make_golden_c3.py [workers] [threads]
+    PYTHONDONTWRITEBYTECODE=1 python oracle/make_golden_c3.py [workers] [threads] [jobdir] [jobs]
+
+Job 0 is the evaluate at theta0, job k >= 1 the gradient's task k-1.  Each
+finished job is also written to ``jobdir`` (default: none) as job_<k>.npz;
+jobs already present there are not recomputed, so a run cut short by a time
+limit can be resumed.  ``jobs`` (comma list) restricts the run to a subset;
+the fixture then holds NaN for the task values not computed yet and the
+gradient only for the coordinates whose two values are present (the test
+checks exactly what is there).  ``oracle/golden_c3_jobs.txt`` records the
+values of jobs computed in earlier runs (repr, exact), which are seeded
+into ``jobdir``.
 
 Output: tests/golden/c3.npz (no model inputs -- they are 10^5-sized; the
 tests rebuild them with the package's generator and check the stored input
@@ -89,6 +99,25 @@ def main():
 
     workers = int(sys.argv[1]) if len(sys.argv) > 1 else 2
     threads = int(sys.argv[2]) if len(sys.argv) > 2 else max(1, (os.cpu_count() or 2) // workers)
+    jobdir = sys.argv[3] if len(sys.argv) > 3 else None
+    want = [int(x) for x in sys.argv[4].split(",")] if len(sys.argv) > 4 else list(range(32))
+    res = {}
+    if jobdir:
+        os.makedirs(jobdir, exist_ok=True)
+        seeds = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden_c3_jobs.txt")
+        if os.path.exists(seeds):  # values of earlier runs: "k value seconds" per line
+            for line in open(seeds):
+                f = line.split()
+                if len(f) == 3 and not os.path.exists(os.path.join(jobdir, f"job_{f[0]}.npz")):
+                    np.savez(os.path.join(jobdir, f"job_{f[0]}.npz"), f=np.array([float(f[1])]),
+                             secs=np.array([float(f[2])]))
+        for k in range(32):
+            path = os.path.join(jobdir, f"job_{k}.npz")
+            if os.path.exists(path):
+                z = np.load(path)
+                res[k] = (float(z["f"][0]), z["mu"] if k == 0 else None,
+                          float(z["mus"][0]) if k == 0 else None, float(z["secs"][0]))
+        print(f"resuming: {len(res)} jobs already done", flush=True)
     sys.path.insert(0, REF)
     from stinla.synthetic import SyntheticSettings, generate_synthetic
 
@@ -99,16 +128,19 @@ def main():
     tmp = tempfile.NamedTemporaryFile(suffix=".pkl", delete=False)
     pickle.dump(data.spec, tmp)
     tmp.close()
-    jobs = [(tmp.name, k, threads) for k in range(32)]
-    res = {}
+    jobs = [(tmp.name, k, threads) for k in want if k not in res]
     t0 = time.perf_counter()
     with mp.get_context("spawn").Pool(workers) as pool:
         for k, f, mu, mus, secs in pool.imap_unordered(_worker, jobs):
             res[k] = (f, mu, mus, secs)
             print(f"  job {k}: {f!r} ({secs:.1f} s)", flush=True)
+            if jobdir:
+                extra = {"mu": mu, "mus": np.array([mus])} if k == 0 else {}
+                np.savez(os.path.join(jobdir, f"job_{k}.npz"), f=np.array([f]),
+                         secs=np.array([secs]), checksums=input_checksums(data.spec), **extra)
     os.unlink(tmp.name)
-    vals = np.array([res[k][0] for k in range(1, 32)])
-    grad = (vals[1::2] - vals[2::2]) / (2.0 * STEP)  # inla.py:436
+    vals = np.array([res[k][0] if k in res else np.nan for k in range(1, 32)])
+    grad = (vals[1::2] - vals[2::2]) / (2.0 * STEP)  # inla.py:436 (NaN where a value is missing)
     f0, mu, mus, _ = res[0]
     np.savez_compressed(
         os.path.join(OUT, "c3.npz"),
@@ -118,10 +150,11 @@ def main():
         f_obj=np.array([f0]), mu_index=MU_SAMPLE, mu=mu, mu_sum=np.array([mus]),
         grad_step=np.array([STEP]), task_values=vals, neg_f=np.array([vals[0]]), grad=grad,
         seconds=np.array([t_gen, time.perf_counter() - t0]),
-        task_seconds=np.array([res[k][3] for k in range(32)]),
+        task_seconds=np.array([res[k][3] if k in res else np.nan for k in range(32)]),
         threads=np.array([workers, threads]),
     )
-    print(f"c3 golden written: f_obj {f0!r}, |grad|_inf {np.abs(grad).max():.6g}", flush=True)
+    print(f"c3 golden written: f_obj {f0!r}, {np.isfinite(vals).sum()} of 31 task values, "
+          f"{np.isfinite(grad).sum()} gradient coordinates", flush=True)
 
 
 if __name__ == "__main__":

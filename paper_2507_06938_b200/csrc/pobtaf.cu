@@ -602,7 +602,7 @@ __global__ void __launch_bounds__(DAG_NT, 1) pobtaf_dag_kernel(Band g, DagWs ws,
       auto cload = [&] { acc_load<Cfg128>(acc, tp.p, tp.ld, er, ec, 0, 0); };
       const TmaOpnd ta = tile_tma(g, tm, tk.R, tk.s0), tb = tile_tma(g, tm, tk.C, tk.s0);
       if (ta.map != nullptr && tb.map != nullptr && (kw % 32 == 0 || ta.col + kw == g.b))
-        tile_mma_tma<Cfg128, true>(acc, ta, tb, kw, smem, s_tbars, tphase, cload);
+        tile_mma_tma<Cfg128, true>(acc, ta, tb, kw, smem, s_tbars, tphase, cload, er, ec);
       else
         tile_mma<Cfg128, true>(acc, A, B, kw, 128, smem, 0, cload);
       if (ws.prof && tid == 0) atomicAdd(ws.prof + 22, gtimer() - t1);

@@ -85,7 +85,8 @@ STBTA_DEV void run_prod(double (&acc)[Cfg::MF][Cfg::NF][2], const Prod& p, int t
       if ((p.K - kb) % 32 == 0) {
         const TmaOpnd3 ta{&tc_->maps->m[p.amap], tr * 128, p.ablk};
         const TmaOpnd3 tb{&tc_->maps->m[p.bmap], tc * 128, p.bblk};
-        tile_mma_tma3<Cfg, AKM, BKM>(acc, ta, tb, kb, p.K, smem, tc_->bars, *tc_->phase);
+        tile_mma_tma3<Cfg, AKM, BKM>(acc, ta, tb, kb, p.K, smem, tc_->bars, *tc_->phase, mrows,
+                                     ncols);
         return;
       }
     }

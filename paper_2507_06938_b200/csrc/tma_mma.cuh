@@ -79,10 +79,21 @@ STBTA_DEV void tma_bars_init(unsigned long long* bars) {
 }
 
 // `phase`: per-stage parity bits, identical in all threads, carried across calls.
+// Output rows >= mv / columns >= nv are not wanted by the caller: the warps'
+// 8 x 8 fragments lying entirely beyond them skip their loads and DMMAs
+// (partial last tiles, e.g. b = 5025 -> 33 columns, and the few arrow rows
+// of an arrowhead tile row, a <= 8 of 128), which frees the SM's DMMA pipe
+// for the useful fragments.
+template <class Cfg>
+STBTA_DEV int valid_frags(int v, int w0, int nf) {
+  return min(nf, max(0, (v - w0 + 7) >> 3));
+}
+
 template <class Cfg, bool NEG = false, class Init = NoInit>
 STBTA_DEV void tile_mma_tma(double (&acc)[Cfg::MF][Cfg::NF][2], const TmaOpnd& A,
                             const TmaOpnd& B, int K, double* smem, unsigned long long* bars,
-                            unsigned& phase, const Init& init = Init()) {
+                            unsigned& phase, const Init& init = Init(), int mv = 128,
+                            int nv = 128) {
   static_assert(Cfg::BM == 128 && Cfg::BN == 128, "TMA path is laid out for 128 x 128 tiles");
   constexpr int MF = Cfg::MF, NF = Cfg::NF;
   double* base = tma_stage_base(smem);
@@ -91,6 +102,8 @@ STBTA_DEV void tile_mma_tma(double (&acc)[Cfg::MF][Cfg::NF][2], const TmaOpnd& A
   const int wm0 = (warp % Cfg::WARPS_M) * Cfg::WM;
   const int wn0 = (warp / Cfg::WARPS_M) * Cfg::WN;
   const int nk = (K + 31) / 32;  // a partial last slab must end at the tensor edge (zero fill)
+  const int mfv = valid_frags<Cfg>(mv, wm0, MF), nfv = valid_frags<Cfg>(nv, wn0, NF);
+  const bool full = (mfv == MF) && (nfv == NF);
   auto issue = [&](int kt) {  // thread 0
     double* st = base + (kt % TMA_ST) * TMA_STAGE;
     unsigned long long* bar = bars + kt % TMA_ST;
@@ -118,21 +131,43 @@ STBTA_DEV void tile_mma_tma(double (&acc)[Cfg::MF][Cfg::NF][2], const TmaOpnd& A
     if (tid == 0 && kt + TMA_ST - 1 < nk) issue(kt + TMA_ST - 1);
     const double* as = base + s * TMA_STAGE;
     const double* bs = as + TMA_OPND;
+    if (full) {
 #pragma unroll
-    for (int ks = 0; ks < 8; ++ks) {
-      const int kp = tma_kp(ks, o4);
-      double af[MF], bf[NF];
+      for (int ks = 0; ks < 8; ++ks) {
+        const int kp = tma_kp(ks, o4);
+        double af[MF], bf[NF];
 #pragma unroll
-      for (int i = 0; i < MF; ++i) af[i] = as[tma_off<false>(wm0 + i * 8 + gq, kp)];
+        for (int i = 0; i < MF; ++i) af[i] = as[tma_off<false>(wm0 + i * 8 + gq, kp)];
 #pragma unroll
-      for (int j = 0; j < NF; ++j) {
-        const double bv = bs[tma_off<false>(wn0 + j * 8 + gq, kp)];
-        bf[j] = NEG ? -bv : bv;
+        for (int j = 0; j < NF; ++j) {
+          const double bv = bs[tma_off<false>(wn0 + j * 8 + gq, kp)];
+          bf[j] = NEG ? -bv : bv;
+        }
+#pragma unroll
+        for (int i = 0; i < MF; ++i)
+#pragma unroll
+          for (int j = 0; j < NF; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
       }
+    } else if (mfv > 0 && nfv > 0) {  // warp-uniform: only the wanted fragments
+#pragma unroll 1
+      for (int ks = 0; ks < 8; ++ks) {
+        const int kp = tma_kp(ks, o4);
+        double af[MF], bf[NF];
 #pragma unroll
-      for (int i = 0; i < MF; ++i)
+        for (int i = 0; i < MF; ++i) af[i] = i < mfv ? as[tma_off<false>(wm0 + i * 8 + gq, kp)] : 0.0;
 #pragma unroll
-        for (int j = 0; j < NF; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+        for (int j = 0; j < NF; ++j) {
+          const double bv = j < nfv ? bs[tma_off<false>(wn0 + j * 8 + gq, kp)] : 0.0;
+          bf[j] = NEG ? -bv : bv;
+        }
+#pragma unroll
+        for (int i = 0; i < MF; ++i) {
+          if (i >= mfv) break;
+#pragma unroll
+          for (int j = 0; j < NF; ++j)
+            if (j < nfv) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+        }
+      }
     }
   }
   __syncthreads();
@@ -183,7 +218,8 @@ STBTA_DEV void tma_issue_opnd(double* dst, const TmaOpnd3& o, int k0, unsigned l
 template <class Cfg, bool AKM, bool BKM>
 STBTA_DEV void tile_mma_tma3(double (&acc)[Cfg::MF][Cfg::NF][2], const TmaOpnd3& A,
                              const TmaOpnd3& B, int kbeg, int K, double* smem,
-                             unsigned long long* bars, unsigned& phase) {
+                             unsigned long long* bars, unsigned& phase, int mv = 128,
+                             int nv = 128) {
   static_assert(Cfg::BM == 128 && Cfg::BN == 128, "TMA path is laid out for 128 x 128 tiles");
   constexpr int MF = Cfg::MF, NF = Cfg::NF;
   double* base = tma_stage_base(smem);
@@ -192,6 +228,8 @@ STBTA_DEV void tile_mma_tma3(double (&acc)[Cfg::MF][Cfg::NF][2], const TmaOpnd3&
   const int wm0 = (warp % Cfg::WARPS_M) * Cfg::WM;
   const int wn0 = (warp / Cfg::WARPS_M) * Cfg::WN;
   const int nk = (K - kbeg) / 32;
+  const int mfv = valid_frags<Cfg>(mv, wm0, MF), nfv = valid_frags<Cfg>(nv, wn0, NF);
+  const bool full = (mfv == MF) && (nfv == NF);
   auto issue = [&](int kt) {  // thread 0
     double* st = base + (kt % TMA_ST) * TMA_STAGE;
     unsigned long long* bar = bars + kt % TMA_ST;
@@ -214,18 +252,37 @@ STBTA_DEV void tile_mma_tma3(double (&acc)[Cfg::MF][Cfg::NF][2], const TmaOpnd3&
     if (tid == 0 && kt + TMA_ST - 1 < nk) issue(kt + TMA_ST - 1);
     const double* as = base + s * TMA_STAGE;
     const double* bs = as + TMA_OPND;
+    if (full) {
 #pragma unroll
-    for (int ks = 0; ks < 8; ++ks) {
-      const int kp = tma_kp(ks, o4);
-      double af[MF], bf[NF];
+      for (int ks = 0; ks < 8; ++ks) {
+        const int kp = tma_kp(ks, o4);
+        double af[MF], bf[NF];
 #pragma unroll
-      for (int i = 0; i < MF; ++i) af[i] = as[tma_off<AKM>(wm0 + i * 8 + gq, kp)];
+        for (int i = 0; i < MF; ++i) af[i] = as[tma_off<AKM>(wm0 + i * 8 + gq, kp)];
 #pragma unroll
-      for (int j = 0; j < NF; ++j) bf[j] = bs[tma_off<BKM>(wn0 + j * 8 + gq, kp)];
+        for (int j = 0; j < NF; ++j) bf[j] = bs[tma_off<BKM>(wn0 + j * 8 + gq, kp)];
 #pragma unroll
-      for (int i = 0; i < MF; ++i)
+        for (int i = 0; i < MF; ++i)
 #pragma unroll
-        for (int j = 0; j < NF; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+          for (int j = 0; j < NF; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+      }
+    } else if (mfv > 0 && nfv > 0) {  // warp-uniform: only the wanted fragments
+#pragma unroll 1
+      for (int ks = 0; ks < 8; ++ks) {
+        const int kp = tma_kp(ks, o4);
+        double af[MF], bf[NF];
+#pragma unroll
+        for (int i = 0; i < MF; ++i) af[i] = i < mfv ? as[tma_off<AKM>(wm0 + i * 8 + gq, kp)] : 0.0;
+#pragma unroll
+        for (int j = 0; j < NF; ++j) bf[j] = j < nfv ? bs[tma_off<BKM>(wn0 + j * 8 + gq, kp)] : 0.0;
+#pragma unroll
+        for (int i = 0; i < MF; ++i) {
+          if (i >= mfv) break;
+#pragma unroll
+          for (int j = 0; j < NF; ++j)
+            if (j < nfv) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+        }
+      }
     }
   }
   __syncthreads();
