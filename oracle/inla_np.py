@@ -141,26 +141,29 @@ def forward_perm(spec):
 
 
 def to_bta(spec, mat):
-    """Dense-free scatter of a symmetric CSR matrix into BTA storage (coreg.py:186-276)."""
+    """Scatter of a symmetric CSR matrix into BTA storage (coreg.py:186-276):
+    entries of the diagonal and first sub-diagonal blocks, the arrow rows
+    and the tip, in the permuted order; vectorised (C3: ~10^7 entries)."""
     nv, ns, nt, nf = spec.n_processes, spec.n_spatial, spec.n_time, spec.n_fixed
     n, b, a = nt, nv * ns, nv * nf
     fwd = forward_perm(spec)
     coo = sp.coo_matrix(mat)
-    pr, pc = fwd[coo.row], fwd[coo.col]
+    pr, pc, v = fwd[coo.row], fwd[coo.col], coo.data
     split = n * b
     data = np.zeros(bta_np.storage_elems(n, b, a))
-    d, lo, ar, tp = bta_np.views(data, n, b, a)
-    for r, c, v in zip(pr, pc, coo.data):
-        if r < split and c < split:
-            ti, tj = r // b, c // b
-            if ti == tj:
-                d[ti][r % b, c % b] = v
-            elif ti == tj + 1:
-                lo[tj][r % b, c % b] = v
-        elif r >= split and c < split:
-            ar[c // b][r - split, c % b] = v
-        elif r >= split and c >= split:
-            tp[r - split, c - split] = v
+    e0 = n * b * b
+    e1 = e0 + (n - 1) * b * b
+    e2 = e1 + n * a * b
+    lat = (pr < split) & (pc < split)
+    ti, tj = pr // b, pc // b
+    m = lat & (ti == tj)
+    data[ti[m] * b * b + (pr[m] % b) * b + pc[m] % b] = v[m]
+    m = lat & (ti == tj + 1)
+    data[e0 + tj[m] * b * b + (pr[m] % b) * b + pc[m] % b] = v[m]
+    m = (pr >= split) & (pc < split)
+    data[e1 + tj[m] * a * b + (pr[m] - split) * b + pc[m] % b] = v[m]
+    m = (pr >= split) & (pc >= split)
+    data[e2 + (pr[m] - split) * a + (pc[m] - split)] = v[m]
     return data, (n, b, a)
 
 
