@@ -402,3 +402,18 @@ def test_gpu_runner_calls_untagged_and_foreign_tasks():
     _, g = inla.fd_gradient(twin, np.array([0.5, 1.0]), 1e-3, runner=runner)
     np.testing.assert_allclose(g, [-1.0, -1.0])
     runner.close()
+
+
+@pytest.mark.parametrize("n,b,a,use_arrow,nfact", [
+    (4, 640, 3, True, -1), (3, 1000, 0, True, -1), (2, 1300, 131, True, -1),
+    (5, 128, 4, True, -1), (3, 897, 2, False, -1), (6, 2048, 6, True, -1),
+    (5, 300, 2, True, -1), (5, 640, 130, True, 3), (4, 300, 2, True, 2)])
+def test_pobtaf_task_graph_order(n, b, a, use_arrow, nfact):
+    """Host model of the POBTAF ticket enumeration (tests/dag_model.py mirrors
+    csrc/pobtaf.cu): every tile of the band gets each panel's update exactly
+    once and in panel order -- per panel, chunked, or merged near updates --
+    and every task's dependencies hold smaller tickets (the persistent
+    kernel's deadlock freedom)."""
+    import dag_model
+
+    assert dag_model.check(dag_model.Band(n, b, a, use_arrow, nfact)) >= 0
