@@ -140,6 +140,9 @@ def main():
                          secs=np.array([secs]), checksums=input_checksums(data.spec), **extra)
     os.unlink(tmp.name)
     vals = np.array([res[k][0] if k in res else np.nan for k in range(1, 32)])
+    if not np.isfinite(vals[0]) and 0 in res:
+        # the gradient's centre task is -objective(theta0) = -(job 0's evaluate f)
+        vals[0] = -res[0][0]
     grad = (vals[1::2] - vals[2::2]) / (2.0 * STEP)  # inla.py:436 (NaN where a value is missing)
     f0, mu, mus, _ = res[0]
     np.savez_compressed(

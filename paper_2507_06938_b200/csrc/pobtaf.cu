@@ -137,28 +137,6 @@ STBTA_DEV bool cross_col(const Band& g, int p, int C) {
   return C >= chunk_end(g, p) + 1 + look(g);
 }
 
-// Merged near updates (left-looking inside the look-ahead window): the tiles
-// (R, C), R >= C + 2, that the panels p in [near_first(C), C - 2] of C - 1's
-// block update one panel at a time (C is "near" for them: not chunked) are
-// instead updated ONCE, by panels near_first(C) .. C - 1, in the task that
-// applies panel C - 1's update (G7(C - 1)); the critical rows (the diagonal
-// tile's strips and row C + 1) stay per panel.  Same products in the same
-// panel order, a fraction of the task count (each task pays a C-tile load /
-// store and a pipeline fill).  Returns C - 1 when nothing is merged.
-STBTA_DEV int near_first(const Band& g, int C) {
-  const int s = C - 1;
-  if (s < 0 || s >= g.n * g.nbt || C >= g.n * g.nbt) return s;
-  const int bs = (s / g.nbt) * g.nbt;
-  const int c = max(C - look(g), bs);
-  return max(chunk_first(g, c), bs);
-}
-
-// Are E(p)'s updates of tile column c below row c + 1 merged into G7(c - 1)?
-STBTA_DEV bool merged_col(const Band& g, int p, int c) {
-  if (p > c - 2 || p >= g.n * g.nbt || cross_col(g, p, c)) return false;
-  return p >= near_first(g, c);
-}
-
 // Does panel p = s-1 update tile (r1, s+1), r1 = second band row of s?  Then
 // that update is hoisted from the bulk (G5) to the front of G4, ahead of
 // panel s's own update of the tile (never chunked: its column is s+1).
@@ -191,10 +169,8 @@ STBTA_DEV int group_size(const Band& g, int kind, int s) {
       const bool last = chunk_last(g, p);
       int e = 0;
       for (int j = 1; j < mp; ++j) {
-        const int c = band_row(g, p, j, mb);
-        if (!last && cross_col(g, p, c)) continue;
-        // merged columns keep only row c + 1 (rows below: G7(c - 1))
-        e += NSTRIP + (merged_col(g, p, c) ? min(1, mp - 1 - j) : (mp - 1 - j));
+        if (!last && cross_col(g, p, band_row(g, p, j, mb))) continue;
+        e += NSTRIP + (mp - 1 - j);
       }
       return e - (g1_active(g, s) ? NSTRIP : 0) - (g4_prev(g, s) ? 1 : 0);
     }
@@ -279,8 +255,6 @@ STBTA_DEV Task decode(const Band& g, const DagWs& ws, int t, int lo) {
       int mb;
       band_rows(g, s, &mb);
       k.type = T_UPD; k.s = s; k.R = band_row(g, s, 2 + local, mb); k.C = s + 1;
-      const int nf = near_first(g, s + 1);
-      k.s0 = nf < s ? nf : -1;  // panels nf..s in one task (merged near updates)
       return k;
     }
     default: break;
@@ -300,8 +274,7 @@ STBTA_DEV Task decode(const Band& g, const DagWs& ws, int t, int lo) {
     k.s0 = cross ? chunk_first(g, p) : p;
     const int ns = (j == 1 && skip) ? 0 : NSTRIP;
     const int hj = j == 1 ? hoist : 0;
-    const int nrow = merged_col(g, p, c) ? min(1, mp - 1 - j) : (mp - 1 - j);
-    const int cnt = ns + nrow - hj;
+    const int cnt = ns + (mp - 1 - j) - hj;
     if (local < cnt) {
       if (local < ns) { k.type = T_STRIP; k.R = k.C = c; k.q = local; return k; }
       k.type = T_UPD;

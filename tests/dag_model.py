@@ -1,5 +1,5 @@
 """Host model of the POBTAF task graph's enumeration (csrc/pobtaf.cu:
-band_rows / band_row / chunking / near_first / merged_col / group_size /
+band_rows / band_row / chunking / group_size /
 decode), used by tests/test_host_logic.py to check on the CPU that the ticket
 order covers every block-tile update exactly once, in panel order, and is a
 topological order of the task dependencies (deadlock freedom of the
@@ -60,21 +60,6 @@ def cross_col(g, p, C):
     return C >= chunk_end(g, p) + 1 + look(g)
 
 
-def near_first(g, C):
-    s = C - 1
-    if s < 0 or s >= g.NB or C >= g.NB:
-        return s
-    bs = (s // g.nbt) * g.nbt
-    c = max(C - look(g), bs)
-    return max(chunk_first(g, c), bs)
-
-
-def merged_col(g, p, c):
-    if p > c - 2 or p >= g.NB or cross_col(g, p, c):
-        return False
-    return p >= near_first(g, c)
-
-
 def g1_active(g, s):
     if s < 1:
         return False
@@ -118,7 +103,7 @@ def group_size(g, kind, s):
             c = band_row(g, p, j, mb)
             if not last and cross_col(g, p, c):
                 continue
-            e += NSTRIP + (min(1, mp - 1 - j) if merged_col(g, p, c) else (mp - 1 - j))
+            e += NSTRIP + (mp - 1 - j)
         return e - (NSTRIP if g1_active(g, s) else 0) - (1 if g4_prev(g, s) else 0)
     if kind == 6:
         return NSTRIP * (m - 2) if m >= 3 else 0
@@ -143,9 +128,7 @@ def decode(g, kind, s, local):
         return ("U", ss, ss, band_row(g, s, 1, mb), s + 1, 0)
     if kind == 7:
         _, mb = band_rows(g, s)
-        nf = near_first(g, s + 1)
-        s0 = nf if nf < s else s
-        return ("U", s0, s, band_row(g, s, 2 + local, mb), s + 1, 0)
+        return ("U", s, s, band_row(g, s, 2 + local, mb), s + 1, 0)
     p = s - 1
     mp, mb = band_rows(g, p)
     skip = g1_active(g, s)
@@ -159,8 +142,7 @@ def decode(g, kind, s, local):
         s0 = chunk_first(g, p) if cross else p
         ns = 0 if (j == 1 and skip) else NSTRIP
         hj = hoist if j == 1 else 0
-        nrow = min(1, mp - 1 - j) if merged_col(g, p, c) else (mp - 1 - j)
-        cnt = ns + nrow - hj
+        cnt = ns + (mp - 1 - j) - hj
         if local < cnt:
             if local < ns:
                 return ("S", s0, p, c, c, local)

@@ -411,7 +411,7 @@ def test_gpu_runner_calls_untagged_and_foreign_tasks():
 def test_pobtaf_task_graph_order(n, b, a, use_arrow, nfact):
     """Host model of the POBTAF ticket enumeration (tests/dag_model.py mirrors
     csrc/pobtaf.cu): every tile of the band gets each panel's update exactly
-    once and in panel order -- per panel, chunked, or merged near updates --
+    once and in panel order -- per panel or chunked --
     and every task's dependencies hold smaller tickets (the persistent
     kernel's deadlock freedom)."""
     import dag_model
