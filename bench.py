@@ -25,8 +25,8 @@ cpu_baseline: the reference's own CPU path -- the UNMODIFIED stinla package
 inla:    the north-star number (BASELINE configs[2]/[3]): measured seconds of
          one BFGS iteration of the trivariate C3 model from theta0 and one
          near the mode over all N GPUs of the run (sched.GpuRunner), with the
-         iteration's useful FP64 TFLOP/s; at N=1 also the reference CPU f_obj
-         of the same model on the host cores.
+         iteration's useful FP64 TFLOP/s.  `--impl reference` at N=1 also
+         times the reference CPU f_obj of the same model on the host cores.
 
 Multi-GPU: `--gpus N` without torchrun re-launches itself through
 torch.distributed.run (one rank per GPU).  Every rank factorizes its own C2
@@ -69,7 +69,13 @@ def parse_args():
     p.add_argument("--config", default="c2", choices=["c2", "c5"],
                    help="c2: BTA microbench (default); c5: distributed POBTAF weak scaling, "
                         "96 time blocks per GPU, one partition per rank over NCCL")
-    p.add_argument("--lb", type=float, default=1.6, help="C5 load-balance factor (plan_partitions lb; 1.6 measured best at 2 and 4 GPUs)")
+    p.add_argument("--lb", type=float, default=2.2,
+                   help="C5 load-balance factor (plan_partitions lb: the first partition, "
+                        "whose blocks cost about 2.2-2.7x less, gets lb times the others' "
+                        "share; 2.2 measured best at 2 and 4 GPUs, profiles/r02_c5_lb_sweep.jsonl)")
+    p.add_argument("--cpu-c3", action="store_true",
+                   help="also time the reference CPU C3 f_obj in this arm (the --impl reference "
+                        "arm does it by default at N=1)")
     p.add_argument("--no-inla", action="store_true",
                    help="skip the C3 north-star measurement (BFGS iterations over the N GPUs)")
     return p.parse_args()
@@ -142,14 +148,6 @@ C3_THETA0 = [-0.35, -0.25, -0.30, -0.20, -0.25, -0.25, 2.05, 2.05, 2.05, 0.05, 0
              -0.35, 0.35]
 C3_TRUE = [-0.40, -0.30, -0.35, -0.25, -0.30, -0.30, 2.00, 2.00, 2.00, 0.00, 0.00, 0.00, 0.60,
            -0.40, 0.30]
-# mode of the C3 mode search (profiles/r01_c3_full_fit_4gpu.json); the "near the
-# mode" iteration starts 5% of the way back towards theta0
-C3_MODE = [-0.40543418642248974, -0.29533394917712885, -0.34564560973639763, -0.23794140115116474,
-           -0.2997964328065215, -0.30007968368004073, 1.9968488287503887, 1.9960265118624916,
-           1.9994540795176827, -0.005057336500345731, 0.008067473509371046, -0.0009885506093976063,
-           0.607928841199783, -0.3901202397773525, 0.29178019168451125]
-
-
 def reference_module():
     """The UNMODIFIED reference package (stinla) installed into baseline/_ref
     (DESIGN.md §4), or None when it is absent (then the oracle port is timed)."""
@@ -224,25 +222,28 @@ class CpuC2:
                 f"untimed; {blas_threads()} BLAS threads")
 
 
-def cpu_c3_fobj(spec):
+def cpu_c3_fobj():
     """One C3 f_obj at theta0 through the reference's own ObjectiveEvaluator
-    (stinla.inla, baseline/_ref) on the host cores, on the model inputs the
-    package generated (byte-identical to the reference generator's, pinned by
-    tests/test_gpu_baseline_configs.py)."""
+    (stinla.inla, baseline/_ref) on the host cores.  The model: the
+    reference's build_spec(settings, default_rng(2)) (the designs: the first
+    draws of generate_synthetic's generator) plus the committed observations
+    bench_data/c3_observations.npz (the package's generator, pinned to the
+    reference's input checksums by tests/test_gpu_baseline_configs.py) --
+    which skips the CPU latent draw (one more C3 POBTAF)."""
     import numpy as np
 
     if reference_module() is None:
         return {"unavailable": "baseline/_ref (reference stinla) not installed"}
     from stinla import inla as ref_inla
-    from stinla.model import ModelSpec as RefSpec
+    from stinla.synthetic import SyntheticSettings, build_spec
 
-    rs = RefSpec(n_processes=spec.n_processes, n_spatial=spec.n_spatial, n_time=spec.n_time,
-                 n_fixed=spec.n_fixed, spatial=spec.spatial, temporal=spec.temporal,
-                 design=spec.design, observations=spec.observations,
-                 fixed_effect_precision=spec.fixed_effect_precision)
+    spec = build_spec(SyntheticSettings(3, 1675, 48, 1, 80400), np.random.default_rng(2))
+    obs = np.load(os.path.join(ROOT, "bench_data", "c3_observations.npz"))
+    spec.observations = [obs[f"y{i}"] for i in range(3)]
+    spec.validate()
     th0 = np.array(C3_THETA0)
     t0 = time.perf_counter()
-    ev = ref_inla.ObjectiveEvaluator(rs, prior=ref_inla.ThetaPrior.for_dim(15, mean=th0, sd=2.0))
+    ev = ref_inla.ObjectiveEvaluator(spec, prior=ref_inla.ThetaPrior.for_dim(15, mean=th0, sd=2.0))
     t_init = time.perf_counter() - t0
     t0 = time.perf_counter()
     f = ev.objective(th0)
@@ -250,7 +251,9 @@ def cpu_c3_fobj(spec):
     return {"kind": "reference", "f_obj_s": t_f, "f_obj": f, "evaluator_init_s": t_init,
             "cores": blas_threads(),
             "sample": "one C3 f_obj at theta0 (reference ObjectiveEvaluator.evaluate, "
-                      "inla.py:320-371), workers=1, all host cores for BLAS"}
+                      "inla.py:320-371), workers=1, all host cores for BLAS",
+            "per_iteration_s_extrapolated": {"from_theta0 (48 f_obj)": 48 * t_f,
+                                             "near_mode (32 f_obj)": 32 * t_f}}
 
 
 def run_reference(args):
@@ -283,20 +286,32 @@ def run_reference(args):
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "seconds_per_step": times,
     }
+    if args.gpus == 1 and not args.no_inla:
+        # the north-star model's f_obj on the same host cores (BASELINE configs[2])
+        del c2, warm
+        try:
+            line["inla_cpu"] = cpu_c3_fobj()
+        except Exception as exc:  # noqa: BLE001 -- the C2 line must still print
+            line["inla_cpu"] = {"error": f"{type(exc).__name__}: {exc}"}
     print(json.dumps(line), flush=True)
     return 0
 
 
 # --------------------------------------------------------------- C3 north star
-def measure_north_star(n_gpus, peak, cpu=True):
+def measure_north_star(n_gpus, peak, cpu=False):
     """The north-star number at N GPUs (BASELINE configs[2]/[3]): seconds per
     BFGS iteration of the trivariate model (n_v=3, n_s=1675, n_t=48; b=5025,
     N=241 203), IterationRecord.seconds of the reference minimize
     (inla.py:535-597) -- Armijo line search + 31-point central-difference
     gradient -- for one iteration from theta0 (far from the mode: many
     backtracking tries) and one started near the mode, one ObjectiveEvaluator
-    per GPU driven by sched.GpuRunner.  Also one f_obj's latency on GPU 0 and,
-    at N = 1, the reference CPU f_obj on the host cores."""
+    per GPU driven by sched.GpuRunner.  Also one f_obj's latency on GPU 0
+    (and with --cpu-c3 at N = 1 the reference CPU f_obj on the host cores,
+    which the --impl reference arm reports by default).  The iterations resume
+    recorded BFGS states of the full C3 fit (bench_data/c3_bfgs_states.npz,
+    tools/c3_fit.py; minimize(state0=...)): state 0 = theta0 with its
+    gradient and an identity inverse Hessian, and the first state near the
+    mode whose next iteration takes one line-search try."""
     import warnings
 
     import numpy as np
@@ -332,38 +347,46 @@ def measure_north_star(n_gpus, peak, cpu=True):
         tc.append(time.perf_counter() - t0)
 
     class Tracked:
-        """Runner wrapper: the work counters after each batch (the first batch
-        of minimize is the starting gradient, outside IterationRecord.seconds)."""
+        """Runner wrapper: the work counters before / after the iteration."""
 
         def __init__(self):
             self.width = runner.width
-            self.marks = []
+            self.rounds = 0
 
         def __call__(self, tasks):
-            out = runner(tasks)
-            self.marks.append(inla.work_counters())
-            return out
+            self.rounds += 1
+            return runner(tasks)
 
-    def one_iteration(start):
+    def one_iteration(theta, state):
+        """One BFGS iteration resumed from a recorded state (minimize state0);
+        IterationRecord.seconds covers the line search + the gradient."""
         inla.prior_cache_clear()
         tr, recs = Tracked(), []
+        w0 = inla.work_counters()
         with warnings.catch_warnings():
             warnings.simplefilter("ignore")
-            inla.minimize(evs[0], start, gtol=1e-3, ftol=1e-8, max_iter=1, runner=tr,
-                          on_iteration=recs.append)
+            inla.minimize(evs[0], theta, gtol=1e-3, ftol=1e-8, max_iter=1, runner=tr,
+                          on_iteration=recs.append, state0=state)
+        w1 = inla.work_counters()
         r = recs[0]
-        w0, w1 = tr.marks[0], tr.marks[-1]
         fl = w1["pobtaf_flops"] - w0["pobtaf_flops"]
-        tries = r.f_evals - 31
-        return {"seconds": r.seconds, "line_search_tries": tries, "f_evals": r.f_evals,
-                "rounds": len(tr.marks) - 1, "pobtaf_completed": w1["pobtaf"] - w0["pobtaf"],
+        return {"seconds": r.seconds, "line_search_tries": r.f_evals - 31, "f_evals": r.f_evals,
+                "rounds": tr.rounds, "pobtaf_completed": w1["pobtaf"] - w0["pobtaf"],
                 "pobtaf_aborted": w1["aborted"] - w0["aborted"],
                 "useful_tflops": fl / r.seconds / 1e12,
                 "frac_of_n_peak": fl / r.seconds / 1e12 / (n_gpus * peak), "f": r.f}
 
-    far = one_iteration(th0)
-    near_start = np.array(C3_MODE) + 0.05 * (th0 - np.array(C3_MODE))
-    near = one_iteration(near_start)
+    st = np.load(os.path.join(ROOT, "bench_data", "c3_bfgs_states.npz"))
+    tries = st["tries"]
+    # near the mode: the first recorded state whose next iteration took 1 try
+    k_near = next(k for k in range(1, len(tries) - 1) if tries[k + 1] == 1)
+
+    def state(k):
+        return st["theta"][k], (st["f"][k], st["grad"][k], st["hinv"][k])
+
+    far = one_iteration(*state(0))
+    near = one_iteration(*state(k_near))
+    far["recorded_state"], near["recorded_state"] = 0, int(k_near)
     runner.close()
     for ev in evs:
         ev.release_workspaces()
@@ -381,13 +404,7 @@ def measure_north_star(n_gpus, peak, cpu=True):
                      "completed POBTAFs of the iteration by the SURVEY §8(d) formula"}
     if cpu and n_gpus == 1:
         try:
-            out["cpu_reference"] = cpu_c3_fobj(data.spec)
-            c = out["cpu_reference"]
-            if "f_obj_s" in c:
-                # same f_obj count as the measured GPU iterations, labelled extrapolated
-                c["iteration_s_extrapolated"] = {
-                    "from_theta0": c["f_obj_s"] * far["f_evals"],
-                    "near_mode": c["f_obj_s"] * near["f_evals"]}
+            out["cpu_reference"] = cpu_c3_fobj()
         except Exception as exc:  # noqa: BLE001 -- the GPU line must still print
             out["cpu_reference"] = {"error": f"{type(exc).__name__}: {exc}"}
     return out
@@ -696,7 +713,7 @@ def main():
         del pristine, ws_f, ws_s, ws_i
         torch.cuda.empty_cache()
         try:
-            inla_obj = measure_north_star(world, peak, cpu=not args.no_cpu)
+            inla_obj = measure_north_star(world, peak, cpu=args.cpu_c3)
         except Exception as exc:  # noqa: BLE001 -- the C2 line must still print
             inla_obj = {"error": f"{type(exc).__name__}: {exc}"}
 

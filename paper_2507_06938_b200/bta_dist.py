@@ -288,8 +288,10 @@ class _Chain:
     left-separator arrowhead rows, d_left / f_left / d_tip in the chain's tip.
 
     Next to it, the original separator-row data the reduced system needs (the
-    left separator's diagonal, arrow and coupling to the previous partition)
-    and the original coupling blocks the partitioned solve multiplies with."""
+    left separator's diagonal, arrow and coupling to the previous partition).
+    The partitioned solve runs through the chain factor itself: one forward
+    and one backward interior sweep, joined to the reduced system by the
+    factor's right-separator link and arrowhead rows."""
 
     def __init__(self, index, lo, hi, left, right, b, a, use_arrow, device):
         self.index, self.lo, self.hi, self.left, self.right = index, lo, hi, left, right
@@ -313,7 +315,6 @@ class _Chain:
         self.info = torch.zeros(1, dtype=torch.int32, device=self.device)
         self.logdet = 0.0
         self.sep_diag = self.sep_lower = self.sep_arrow = None
-        self.cpl_left = self.cpl_right = self.arrow_int = None
 
     def load(self, rows):
         """Fill the chain from block rows [start, end) (BTARows or a global
@@ -331,13 +332,10 @@ class _Chain:
             self.diag[ni].copy_(g(rows.d(hi)))
             if ni > 0:
                 self.lower[ni - 1].copy_(g(rows.low(hi)))
-                self.cpl_right = g(rows.low(hi)).clone()
         if self.left is not None:
             # A(left, lo) = A(lo, left)^T; with an empty interior this is the
             # original A(left, right)^T -- the fill the reduced system reads
             self.arrow[0, :b].copy_(g(rows.low(lo)).T)
-            if ni > 0:
-                self.cpl_left = g(rows.low(lo)).clone()
             t = self.left
             self.sep_diag = g(rows.d(t)).clone()
             self.sep_lower = g(rows.low(t)).clone() if t > 0 else None
@@ -345,9 +343,7 @@ class _Chain:
                 self.sep_arrow = g(rows.arw(t)).clone()
         if self.a > 0 and self.use_arrow:
             if ni > 0:
-                ar = g(rows.arrow[lo - rows.t0 : hi - rows.t0])
-                self.arrow[:ni, self.off :].copy_(ar)
-                self.arrow_int = ar.clone()
+                self.arrow[:ni, self.off :].copy_(g(rows.arrow[lo - rows.t0 : hi - rows.t0]))
             if self.right is not None:
                 self.arrow[ni, self.off :].copy_(g(rows.arw(hi)))
         return self
@@ -419,8 +415,9 @@ class _Chain:
         return torch.cat([parts[name].reshape(-1) for name, _ in layout])
 
     # -- partitioned solve -----------------------------------------------------
-    def interior_solve(self, rhs):
-        """In place: rhs (n_int*b, k) := A_int^{-1} rhs with the interior factor."""
+    def interior_sweep(self, rhs, mode):
+        """In place on rhs (n_int*b, k) with the interior factor L_int:
+        mode 1: L_int y = rhs (forward), mode 2: L_int^T x = rhs (backward)."""
         lib = _lib.load()
         n, b = self.n_int, self.b
         k = rhs.shape[1]
@@ -428,49 +425,55 @@ class _Chain:
             ws = bta._workspace(lib.stbta_pobtas_workspace_bytes(n, b, 0, k), self.device)
             _lib.check(
                 lib.stbta_pobtas_ex(_lib.ptr(self.diag), _lib.ptr(self.lower), None, None, n, b, 0,
-                                    b, 0, _lib.ptr(rhs), k, 0, _lib.ptr(ws), ws.numel(),
+                                    b, 0, _lib.ptr(rhs), k, mode, _lib.ptr(ws), ws.numel(),
                                     _lib.stream_ptr()),
                 "stbta_pobtas_ex",
             )
         return rhs
 
     def solve_forward(self, xr):
-        """xr: this partition's right-hand-side rows [start, end) (rows*b, k) on
-        this device.  Returns (z, contribution): z = A_int^-1 x_int and the
-        flat [x_left - A(left,lo) z_lo | x_right - A(hi,hi-1) z_last |
-        -sum_j A(arrow, j) z_j] (the parts that exist)."""
+        """Forward half of the partitioned solve through the chain factor
+        (bta_dist.py:370-420): y_int = L_int^-1 x_int, then the extended rows'
+        reduced right-hand sides r_ext - L_ext,int y_int, with L_ext,int the
+        right separator's link L(hi, hi-1) and the arrowhead rows (left
+        separator + arrow) of the factor.  xr: this partition's rows [start,
+        end) (rows*b, k) on this device.  Returns (y_int, flat [c_left |
+        c_right | c_tip]) (the parts that exist)."""
         b = self.b
         k = xr.shape[1]
         i0 = (self.lo - self.start) * b
-        z = xr[i0 : i0 + self.n_int * b].clone()
+        y = xr[i0 : i0 + self.n_int * b].clone()
         out = []
         with torch.cuda.device(self.device):
+            s_ah = None
             if self.n_int:
-                self.interior_solve(z)
+                self.interior_sweep(y, 1)
+                if self.chain_arrow:  # sum_j L(arrowhead, j) y_j, j over the interior
+                    s_ah = torch.zeros(self.ap, k, dtype=torch.float64, device=self.device)
+                    _couple(0, self.arrow[: self.n_int, : self.ap], y.view(self.n_int, b, k),
+                            s_ah, 1.0, reduce=True)
             if self.left is not None:
                 c = xr[:b].clone()
-                if self.n_int:
-                    _couple(1, self.cpl_left, z[:b], c, -1.0)
+                if s_ah is not None:
+                    c -= s_ah[:b]
                 out.append(c)
             if self.right is not None:
                 c = xr[(self.end - 1 - self.start) * b :].clone()
                 if self.n_int:
-                    _couple(0, self.cpl_right, z[-b:], c, -1.0)
+                    _couple(0, self.lower[self.n_int - 1], y[-b:], c, -1.0)
                 out.append(c)
             if self.use_arrow and self.a:
-                c = torch.zeros(self.a, k, dtype=torch.float64, device=self.device)
-                if self.n_int:
-                    _couple(0, self.arrow_int, z.view(self.n_int, b, k), c, -1.0, reduce=True)
-                out.append(c)
+                out.append(-s_ah[self.off :] if s_ah is not None else
+                           torch.zeros(self.a, k, dtype=torch.float64, device=self.device))
         flat = torch.cat([c.reshape(-1) for c in out]) if out else \
             torch.zeros(0, dtype=torch.float64, device=self.device)
-        return z, flat
+        return y, flat
 
-    def solve_backward(self, z, x_left, x_right, x_tip):
-        """Interior solution x_int = z - A_int^-1 (couplings . separator / tip
-        solutions); returns this partition's solution rows [start, end)."""
+    def solve_backward(self, y, x_left, x_right, x_tip):
+        """x_int = L_int^-T (y_int - L_ext,int^T x_ext); returns this
+        partition's solution rows [start, end)."""
         b = self.b
-        k = z.shape[1]
+        k = y.shape[1]
         with torch.cuda.device(self.device):
             rows = torch.empty((self.end - self.start) * b, k, dtype=torch.float64,
                                device=self.device)
@@ -479,17 +482,20 @@ class _Chain:
             if self.right is not None:
                 rows[(self.end - 1 - self.start) * b :] = x_right
             if self.n_int:
-                w = torch.zeros(self.n_int * b, k, dtype=torch.float64, device=self.device)
-                if self.left is not None:
-                    _couple(0, self.cpl_left, x_left, w[:b])
+                w = y.clone()
                 if self.right is not None:
-                    _couple(1, self.cpl_right, x_right, w[-b:])
-                if self.use_arrow and self.a:
-                    _couple(1, self.arrow_int, x_tip.expand(self.n_int, self.a, k),
-                            w.view(self.n_int, b, k))
-                self.interior_solve(w)
+                    _couple(1, self.lower[self.n_int - 1], x_right, w[-b:], -1.0)
+                if self.chain_arrow:
+                    x_ah = torch.zeros(self.ap, k, dtype=torch.float64, device=self.device)
+                    if self.left is not None:
+                        x_ah[:b] = x_left
+                    if self.a > 0 and x_tip is not None:
+                        x_ah[self.off :] = x_tip
+                    _couple(1, self.arrow[: self.n_int, : self.ap],
+                            x_ah.expand(self.n_int, self.ap, k), w.view(self.n_int, b, k), -1.0)
+                self.interior_sweep(w, 2)
                 i0 = (self.lo - self.start) * b
-                rows[i0 : i0 + self.n_int * b] = z - w
+                rows[i0 : i0 + self.n_int * b] = w
         return rows
 
     # -- partitioned selected inversion ------------------------------------

@@ -945,12 +945,14 @@ def minimize(objective, theta0, gtol=1e-3, ftol=1e-6, max_iter=100, grad_step=1e
             direction = -grad
             slope = -float(grad @ grad)
         step, accepted, tries = 1.0, False, 0
-        width = int(getattr(runner, "width", 1)) if runner is not None else 1
-        if width > 1:
+        width = max(1, int(getattr(runner, "width", 1))) if runner is not None else 1
+        if runner is not None:
             # Armijo backtracking with the next `width` step sizes evaluated
-            # concurrently (one per GPU); the first acceptable one in
-            # backtracking order is taken, so the accepted step, theta and
-            # the sequential try count are exactly those of the loop below.
+            # concurrently through the runner (one per GPU or GPU pair; width
+            # 1 still lets the runner split an f_obj over a GPU pair); the
+            # first acceptable one in backtracking order is taken, so the
+            # accepted step, theta and the sequential try count are exactly
+            # those of the loop below.
             k, st = 0, 1.0
             while k <= max_backtracks and not accepted:
                 ks = list(range(k, min(k + width, max_backtracks + 1)))
