@@ -18,9 +18,6 @@
 //      substitution + block updates) and publishes the tile (release flag).
 // The arrow rows become per-tile partial products summed in tile order by the
 // tip kernel, which also solves L_tip (reference bta.py:263-273, 288-300).
-// The neighbour's coupling term is pushed with the flag and formed in the
-// same pass as the tile's own solution from a precomputed product
-// (push_prod_kernel), so the critical step per tile is one 128-row pass.
 #include "../../include/stbta.h"
 #include "band.cuh"
 #include "common.cuh"
@@ -58,7 +55,6 @@ struct SweepArgs {
   double* push;   // [ntile][128][NR]: coupling contribution pushed to the next tile
   unsigned long long* prof;  // optional debug timers (slots 20..23)
   const double* winv;  // [ntile][WPK]: packed inverses of the diagonal tiles
-  const double* mprod; // [ntile][128*128]: coupling x inverse products (push_kernel)
 };
 
 // ---------------------------------------------------------------- pre-pass
@@ -86,85 +82,6 @@ __global__ void __launch_bounds__(PS_NT, 1) inv_tiles_kernel(Band g, double* win
     if ((r + 1) * (r + 2) / 2 <= e) ++r;
     if (r * (r + 1) / 2 > e) --r;
     out[e] = inv_tile_at(sm, r, e - r * (r + 1) / 2);
-  }
-}
-
-// Push products: the tile that solves block row R also hands its neighbour
-// the coupling term, and that term is a fixed matrix times R's right-hand
-// side accumulator, so it is precomputed once per factorization:
-//   forward   u_{R+1} = L_{R+1,R} y_R = (L_{R+1,R} W_R) acc_R   -> M_R, stored transposed
-//   backward  v_{R-1} = L_{R,R-1}^T x_R = (W_R L_{R,R-1})^T acc_R -> N_R, stored row-major
-// (W_R = L_RR^-1).  The sweep then forms y_R and the push in ONE pass over
-// acc_R, with the product prefetched into registers before the tile's
-// neighbour publishes -- no 128 KB coupling block load on the critical step.
-// Layout: mprod[R][q * 128 + r] is the coefficient of acc_R[q] in the push's
-// row r, so the sweep's thread (r, half) reads consecutive addresses.
-constexpr int PP_LD = 129;
-constexpr int PP_SMEM_DOUBLES = WPK + 128 * PP_LD;
-
-template <bool FWD>
-__global__ void __launch_bounds__(PS_NT, 1) push_prod_kernel(Band g, const double* winv,
-                                                              double* mprod, int ntile) {
-  extern __shared__ __align__(16) double sm[];
-  double* Wp = sm;         // packed W_R
-  double* Ls = sm + WPK;   // coupling tile, 128 x PP_LD
-  const int R = blockIdx.x;
-  const int tid = threadIdx.x;
-  double* out = mprod + (long long)R * 128 * 128;
-  const bool has = FWD ? (R + 1 < ntile) : (R >= 1);
-  if (!has) return;
-  const double* src = winv + (long long)R * WPK;
-  for (int e = tid; e < WPK; e += PS_NT) Wp[e] = src[e];
-  // FWD: L = tile (R+1, R): rows of R+1, cols of R.  BWD: L = tile (R, R-1).
-  const TilePtr t = FWD ? tile_ptr(g, R + 1, R) : tile_ptr(g, R, R - 1);
-  const int nr = FWD ? tile_extent(g, R + 1) : tile_extent(g, R);
-  const int nc = FWD ? tile_extent(g, R) : tile_extent(g, R - 1);
-  for (int e = tid; e < 128 * 128; e += PS_NT) {
-    const int r = e >> 7, c = e & 127;
-    Ls[r * PP_LD + c] = (r < nr && c < nc) ? __ldg(t.p + (long long)r * t.ld + c) : 0.0;
-  }
-  __syncthreads();
-  // thread -> 8 x 8 output block: a0 = (tid & 15) * 8 (fast index), b0 = (tid >> 4) * 8
-  const int a0 = (tid & 15) * 8, b0 = (tid >> 4) * 8;
-  double acc[8][8];
-#pragma unroll
-  for (int i = 0; i < 8; ++i)
-#pragma unroll
-    for (int j = 0; j < 8; ++j) acc[i][j] = 0.0;
-  if (FWD) {
-    // MT[q][r] = M[r][q] = sum_{k >= q} L[r][k] W[k][q];  r = a0 + i, q = b0 + j
-    for (int k = b0; k < 128; ++k) {
-      double lv[8], wv[8];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) lv[i] = Ls[(a0 + i) * PP_LD + k];
-#pragma unroll
-      for (int j = 0; j < 8; ++j) wv[j] = (b0 + j <= k) ? Wp[pk(k, b0 + j)] : 0.0;
-#pragma unroll
-      for (int i = 0; i < 8; ++i)
-#pragma unroll
-        for (int j = 0; j < 8; ++j) acc[i][j] = fma(lv[i], wv[j], acc[i][j]);
-    }
-#pragma unroll
-    for (int j = 0; j < 8; ++j)
-#pragma unroll
-      for (int i = 0; i < 8; ++i) out[(b0 + j) * 128 + a0 + i] = acc[i][j];
-  } else {
-    // N[q][r] = sum_{k <= q} W[q][k] L[k][r];  r = a0 + i, q = b0 + j
-    for (int k = 0; k < b0 + 8; ++k) {
-      double lv[8], wv[8];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) lv[i] = Ls[k * PP_LD + a0 + i];
-#pragma unroll
-      for (int j = 0; j < 8; ++j) wv[j] = (k <= b0 + j) ? Wp[pk(b0 + j, k)] : 0.0;
-#pragma unroll
-      for (int i = 0; i < 8; ++i)
-#pragma unroll
-        for (int j = 0; j < 8; ++j) acc[i][j] = fma(wv[j], lv[i], acc[i][j]);
-    }
-#pragma unroll
-    for (int j = 0; j < 8; ++j)
-#pragma unroll
-      for (int i = 0; i < 8; ++i) out[(b0 + j) * 128 + a0 + i] = acc[i][j];
   }
 }
 
@@ -278,17 +195,6 @@ __global__ void __launch_bounds__(PS_NT, 1) sweep_kernel(SweepArgs p) {
     cp_async_commit();
   }
 
-  // the push product (this tile's half of it) into registers: it is needed
-  // only after the neighbour publishes, so its load is off the critical step
-  const int pushto = FWD ? ((R + 1 < p.ntile) ? R + 1 : -1) : R - 1;
-  double mreg[64];
-  {
-    const int r_ = tid & 127, h_ = tid >> 7;
-    const double* mp = p.mprod + (long long)R * 128 * 128 + (long long)(h_ * 64) * 128 + r_;
-#pragma unroll
-    for (int qq = 0; qq < 64; ++qq) mreg[qq] = pushto >= 0 ? __ldcg(mp + qq * 128) : 0.0;
-  }
-
   // pulled dependencies: forward k in [lo, R-1) ascending; backward k in (R+1, hi] descending
   // (the adjacent tile is pushed: it sends its coupling product with its flag)
   int kfirst, nk, crit;
@@ -378,6 +284,21 @@ __global__ void __launch_bounds__(PS_NT, 1) sweep_kernel(SweepArgs p) {
   __syncthreads();
   if (p.prof && tid == 0) t1 = pt_timer();
 
+  // prefetch the push block: forward tile (R+1, R) [rows of R+1 x cols of R],
+  // backward tile (R, R-1) [rows of R x cols of R-1]
+  const int pushto = FWD ? ((R + 1 < p.ntile) ? R + 1 : -1) : R - 1;
+  if (pushto >= 0) {
+    const TilePtr t = FWD ? tile_ptr(g, R + 1, R) : tile_ptr(g, R, R - 1);
+    const int nr = FWD ? tile_extent(g, R + 1) : extR;
+    const int ncl = FWD ? extR : tile_extent(g, R - 1);
+    for (int e = tid; e < 128 * 128; e += PS_NT) {
+      const int rr = e >> 7, cc = e & 127;
+      if (rr < nr && cc < ncl) cp_async8(Pb + rr * P_LD + cc, t.p + (long long)rr * t.ld + cc, true);
+      else Pb[rr * P_LD + cc] = 0.0;
+    }
+  }
+  cp_async_commit();
+
   // accb = rhs + pulled contributions (h0 then h1, fixed order)
   if (h == 0) {
 #pragma unroll
@@ -404,41 +325,19 @@ __global__ void __launch_bounds__(PS_NT, 1) sweep_kernel(SweepArgs p) {
   cp_async_wait<0>();
   __syncthreads();
   if (p.prof && tid == 0) t2 = pt_timer();
-  // one pass over acc: y = W acc (forward) / x = W^T acc (backward) into
-  // ybuf and the push  u = M acc / v = N^T acc  (M, N from registers)
-  {
-    double sy[NRC], su[NRC];
-#pragma unroll
-    for (int c = 0; c < NRC; ++c) sy[c] = su[c] = 0.0;
-#pragma unroll
-    for (int qq = 0; qq < 64; ++qq) {  // fully unrolled: mreg stays in registers
-      const int q = h * 64 + qq;
-      const double w = FWD ? (q <= r ? Wp[pk(r, q)] : 0.0) : (q >= r ? Wp[pk(q, r)] : 0.0);
-      const double m = mreg[qq];
-      const double* aq = accb + q * NR;
-#pragma unroll
-      for (int c = 0; c < NRC; ++c) {
-        sy[c] = fma(w, aq[c], sy[c]);
-        su[c] = fma(m, aq[c], su[c]);
-      }
-    }
-    double* tmp = Pb;  // the ring is drained: 2 x 128 x NR partial sums
-    if (h == 1) {
-#pragma unroll
-      for (int c = 0; c < NRC; ++c) {
-        tmp[r * NR + c] = sy[c];
-        tmp[128 * NR + r * NR + c] = su[c];
-      }
-    }
-    __syncthreads();
-    if (h == 0) {
-#pragma unroll
-      for (int c = 0; c < NRC; ++c) {
-        ybuf[r * NR + c] = sy[c] + tmp[r * NR + c];
-        if (pushto >= 0) p.push[(long long)pushto * 128 * NR + r * NR + c] = su[c] + tmp[128 * NR + r * NR + c];
-      }
-    }
-    __syncthreads();
+  // y = W acc (forward)  /  x = W^T acc (backward); result in ybuf
+  if (FWD)
+    gemv128<NRC>(ybuf, accb, ybuf, [&](int rr, int q) { return q <= rr ? Wp[pk(rr, q)] : 0.0; });
+  else
+    gemv128<NRC>(ybuf, accb, ybuf, [&](int rr, int q) { return q >= rr ? Wp[pk(q, rr)] : 0.0; });
+  // push: forward u = L_{R+1,R} y  ->  push[R+1];  backward v = L_{R,R-1}^T x -> push[R-1]
+  if (pushto >= 0) {
+    if (FWD)
+      gemv128<NRC>(accb, ybuf, accb, [&](int rr, int q) { return Pb[rr * P_LD + q]; });
+    else
+      gemv128<NRC>(accb, ybuf, accb, [&](int rr, int q) { return Pb[q * P_LD + rr]; });
+    double* dst = p.push + (long long)pushto * 128 * NR;
+    for (int e = tid; e < 128 * NR; e += PS_NT) dst[e] = accb[e];
   }
   // publish the solution
   for (int e = tid; e < extR * NR; e += PS_NT) {
@@ -522,7 +421,6 @@ struct PobtasWs {
   double* xtip;
   double* push;
   double* winv;
-  double* mprod;
 };
 
 static size_t pobtas_ws(int n, int b, int a, char* base, PobtasWs* o) {
@@ -531,8 +429,7 @@ static size_t pobtas_ws(int n, int b, int a, char* base, PobtasWs* o) {
   const size_t pa = align_up((size_t)ntile * (a > 0 ? a : 1) * NR * sizeof(double));
   const size_t xt = align_up((size_t)(a > 0 ? a : 1) * NR * sizeof(double));
   const size_t pu = align_up((size_t)ntile * 128 * NR * sizeof(double));
-  const size_t wi = align_up((size_t)ntile * WPK * sizeof(double));
-  const size_t mp = (size_t)ntile * 128 * 128 * sizeof(double);
+  const size_t wi = (size_t)ntile * WPK * sizeof(double);
   if (o) {
     o->flags = reinterpret_cast<int*>(base);
     o->ticket = o->flags + ntile;
@@ -540,9 +437,8 @@ static size_t pobtas_ws(int n, int b, int a, char* base, PobtasWs* o) {
     o->xtip = reinterpret_cast<double*>(base + f + pa);
     o->push = reinterpret_cast<double*>(base + f + pa + xt);
     o->winv = reinterpret_cast<double*>(base + f + pa + xt + pu);
-    o->mprod = reinterpret_cast<double*>(base + f + pa + xt + pu + wi);
   }
-  return f + pa + xt + pu + wi + mp;
+  return f + pa + xt + pu + wi;
 }
 
 static int run_sweeps(SweepArgs p, int mode, const PobtasWs& ws, cudaStream_t st) {
@@ -561,11 +457,6 @@ static int run_sweeps(SweepArgs p, int mode, const PobtasWs& ws, cudaStream_t st
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int e3 = (int)cudaFuncSetAttribute(inv_tiles_kernel,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ismem);
-    const int psm = (int)(PP_SMEM_DOUBLES * sizeof(double));
-    e3 |= (int)cudaFuncSetAttribute(push_prod_kernel<true>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, psm);
-    e3 |= (int)cudaFuncSetAttribute(push_prod_kernel<false>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, psm);
     if (e1) return e1;
     if (e2) return e2;
     if (e3) return e3;
@@ -575,11 +466,7 @@ static int run_sweeps(SweepArgs p, int mode, const PobtasWs& ws, cudaStream_t st
   inv_tiles_kernel<<<p.ntile, PS_NT, ismem, st>>>(p.g, ws.winv);
   count_launch();
   if ((e = (int)cudaGetLastError())) return e;
-  const size_t psmem = PP_SMEM_DOUBLES * sizeof(double);
   if (mode == 0 || mode == 1) {
-    push_prod_kernel<true><<<p.ntile, PS_NT, psmem, st>>>(p.g, ws.winv, ws.mprod, p.ntile);
-    count_launch();
-    if ((e = (int)cudaGetLastError())) return e;
     if ((e = zero_async(p.flags, fbytes, st))) return e;
     if (p.ncols == 1) sweep_kernel<true, 1><<<p.ntile, PS_NT, smem, st>>>(p);
     else sweep_kernel<true, NR><<<p.ntile, PS_NT, smem, st>>>(p);
@@ -597,9 +484,6 @@ static int run_sweeps(SweepArgs p, int mode, const PobtasWs& ws, cudaStream_t st
       count_launch();
       if ((e = (int)cudaGetLastError())) return e;
     }
-    push_prod_kernel<false><<<p.ntile, PS_NT, psmem, st>>>(p.g, ws.winv, ws.mprod, p.ntile);
-    count_launch();
-    if ((e = (int)cudaGetLastError())) return e;
     if ((e = zero_async(p.flags, fbytes, st))) return e;
     if (p.ncols == 1) sweep_kernel<false, 1><<<p.ntile, PS_NT, smem, st>>>(p);
     else sweep_kernel<false, NR><<<p.ntile, PS_NT, smem, st>>>(p);
@@ -668,7 +552,6 @@ int stbta_pobtas_ex(const double* diag, const double* lower, const double* arrow
   p.xtip = ws.xtip;
   p.push = ws.push;
   p.winv = ws.winv;
-  p.mprod = ws.mprod;
   p.prof = debug_profile();
   for (int c0 = 0; c0 < nrhs; c0 += NR) {
     p.x = rhs + c0;
