@@ -105,6 +105,11 @@ def main():
     if jobdir:
         os.makedirs(jobdir, exist_ok=True)
         seeds = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden_c3_jobs.txt")
+        job0 = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden_c3_job0.npz")
+        if os.path.exists(job0) and not os.path.exists(os.path.join(jobdir, "job_0.npz")):
+            z = np.load(job0)  # the evaluate at theta0 (f, sampled mean) of an earlier run
+            np.savez(os.path.join(jobdir, "job_0.npz"), f=z["f"], mu=z["mu"], mus=z["mus"],
+                     secs=z["secs"])
         if os.path.exists(seeds):  # values of earlier runs: "k value seconds" per line
             for line in open(seeds):
                 f = line.split()
