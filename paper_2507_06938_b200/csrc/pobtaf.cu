@@ -137,6 +137,23 @@ STBTA_DEV bool cross_col(const Band& g, int p, int C) {
   return C >= chunk_end(g, p) + 1 + look(g);
 }
 
+// How panel p's update of tile column C is issued:
+//   1  per panel (the last LOOK panels before C, and arrow panels),
+//   2  as part of a chunk task (s0 = chunk_first(p)) issued at this panel:
+//      an aligned chunk at its last panel when all of it is >= LOOK panels
+//      before C, else the remainder [chunk_first(p), C - LOOK - 1] at panel
+//      C - LOOK - 1 -- so every column gets at most LOOK single-panel
+//      updates, each issued LOOK panels ahead of its use,
+//   0  not at this panel (it is in a chunk task issued elsewhere).
+// The remainder chunks only pay for wide blocks (the C3 block size: 1.6% on
+// POBTAF); with narrow ones (C2) the window is all per-panel, as before.
+STBTA_DEV int col_mode(const Band& g, int p, int C) {
+  if (p >= g.n * g.nbt) return 1;
+  if (cross_col(g, p, C)) return chunk_last(g, p) ? 2 : 0;
+  if (C <= p + look(g) || g.nbt < 24) return 1;
+  return p == C - look(g) - 1 ? 2 : 0;
+}
+
 // Does panel p = s-1 update tile (r1, s+1), r1 = second band row of s?  Then
 // that update is hoisted from the bulk (G5) to the front of G4, ahead of
 // panel s's own update of the tile (never chunked: its column is s+1).
@@ -166,10 +183,9 @@ STBTA_DEV int group_size(const Band& g, int kind, int s) {
       if (s < 1) return 0;
       const int p = s - 1;
       const int mp = band_rows(g, p, &mb);
-      const bool last = chunk_last(g, p);
       int e = 0;
       for (int j = 1; j < mp; ++j) {
-        if (!last && cross_col(g, p, band_row(g, p, j, mb))) continue;
+        if (col_mode(g, p, band_row(g, p, j, mb)) == 0) continue;
         e += NSTRIP + (mp - 1 - j);
       }
       return e - (g1_active(g, s) ? NSTRIP : 0) - (g4_prev(g, s) ? 1 : 0);
@@ -265,13 +281,12 @@ STBTA_DEV Task decode(const Band& g, const DagWs& ws, int t, int lo) {
   const int mp = band_rows(g, p, &mb);
   const bool skip = g1_active(g, s);
   const int hoist = g4_prev(g, s) ? 1 : 0;  // UPDATE(p, band_row 2, band_row 1) is in G4
-  const bool last = chunk_last(g, p);
   k.s = p;
   for (int j = 1; j < mp; ++j) {
     const int c = band_row(g, p, j, mb);
-    const bool cross = cross_col(g, p, c);
-    if (cross && !last) continue;
-    k.s0 = cross ? chunk_first(g, p) : p;
+    const int mode = col_mode(g, p, c);
+    if (mode == 0) continue;
+    k.s0 = mode == 2 ? chunk_first(g, p) : p;
     const int ns = (j == 1 && skip) ? 0 : NSTRIP;
     const int hj = j == 1 ? hoist : 0;
     const int cnt = ns + (mp - 1 - j) - hj;

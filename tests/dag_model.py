@@ -60,6 +60,17 @@ def cross_col(g, p, C):
     return C >= chunk_end(g, p) + 1 + look(g)
 
 
+def col_mode(g, p, c):
+    """1 per panel, 2 chunk task at this panel, 0 elsewhere (pobtaf.cu col_mode)."""
+    if p >= g.NB:
+        return 1
+    if cross_col(g, p, c):
+        return 2 if chunk_last(g, p) else 0
+    if c <= p + look(g) or g.nbt < 24:
+        return 1
+    return 2 if p == c - look(g) - 1 else 0
+
+
 def g1_active(g, s):
     if s < 1:
         return False
@@ -97,11 +108,9 @@ def group_size(g, kind, s):
             return 0
         p = s - 1
         mp, mb = band_rows(g, p)
-        last = chunk_last(g, p)
         e = 0
         for j in range(1, mp):
-            c = band_row(g, p, j, mb)
-            if not last and cross_col(g, p, c):
+            if col_mode(g, p, band_row(g, p, j, mb)) == 0:
                 continue
             e += NSTRIP + (mp - 1 - j)
         return e - (NSTRIP if g1_active(g, s) else 0) - (1 if g4_prev(g, s) else 0)
@@ -133,13 +142,12 @@ def decode(g, kind, s, local):
     mp, mb = band_rows(g, p)
     skip = g1_active(g, s)
     hoist = 1 if g4_prev(g, s) else 0
-    last = chunk_last(g, p)
     for j in range(1, mp):
         c = band_row(g, p, j, mb)
-        cross = cross_col(g, p, c)
-        if cross and not last:
+        mode = col_mode(g, p, c)
+        if mode == 0:
             continue
-        s0 = chunk_first(g, p) if cross else p
+        s0 = chunk_first(g, p) if mode == 2 else p
         ns = 0 if (j == 1 and skip) else NSTRIP
         hj = hoist if j == 1 else 0
         cnt = ns + (mp - 1 - j) - hj

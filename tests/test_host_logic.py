@@ -407,11 +407,12 @@ def test_gpu_runner_calls_untagged_and_foreign_tasks():
 @pytest.mark.parametrize("n,b,a,use_arrow,nfact", [
     (4, 640, 3, True, -1), (3, 1000, 0, True, -1), (2, 1300, 131, True, -1),
     (5, 128, 4, True, -1), (3, 897, 2, False, -1), (6, 2048, 6, True, -1),
-    (5, 300, 2, True, -1), (5, 640, 130, True, 3), (4, 300, 2, True, 2)])
+    (5, 300, 2, True, -1), (5, 640, 130, True, 3), (4, 300, 2, True, 2),
+    (3, 3072, 6, True, -1), (2, 3100, 3, True, 1)])
 def test_pobtaf_task_graph_order(n, b, a, use_arrow, nfact):
     """Host model of the POBTAF ticket enumeration (tests/dag_model.py mirrors
     csrc/pobtaf.cu): every tile of the band gets each panel's update exactly
-    once and in panel order -- per panel or chunked --
+    once and in panel order -- per panel, aligned chunks or remainder chunks --
     and every task's dependencies hold smaller tickets (the persistent
     kernel's deadlock freedom)."""
     import dag_model
