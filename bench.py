@@ -722,7 +722,7 @@ def main():
         dom = "pobtasi" if t_i > t_f else "pobtaf"
         achieved = (f_i / t_i if dom == "pobtasi" else f_f / t_f) / 1e12
         traffic = None
-        tpath = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01_traffic.json")
+        tpath = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r02_traffic.json")
         if os.path.exists(tpath) and (n, b, a) == (48, 2048, 6):
             with open(tpath) as fh:
                 traffic = json.load(fh).get(f"c2_{dom}", {}).get("dram_bytes")
@@ -737,7 +737,7 @@ def main():
             "roofline": {"bound": "tensor", "kernel": kname,
                          "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "traffic_unit": "DRAM bytes per call (ncu, profiles/r01_traffic.json)",
+                         "traffic_unit": "DRAM bytes per call (ncu --set full, profiles/r02_traffic.json)",
                          "peak_source": "FP64 DMMA.8x8x4 register-loop probe measured live "
                                         "(MEASURED_PEAKS.json has no FP64 entry)"},
             "routines": {
