@@ -37,6 +37,9 @@ struct Band {
   int use_arrow; // arrow rows take part in the block eliminations
   int vec_b;     // b even: rows of diag/lower/arrow are 16-byte aligned
   int vec_a;     // tip rows 16-byte aligned (a even and b even)
+  int chunk;     // POBTAF: panels per chunked update (0: default by block width)
+  int look;      // POBTAF: per-panel look-ahead window (0: default)
+  int remainder; // POBTAF: remainder chunks inside the window (-1: default)
 };
 
 STBTA_DEV bool is_arrow_tile(const Band& g, int R) { return R >= g.n * g.nbt; }

@@ -122,8 +122,11 @@ STBTA_DEV bool g1_active(const Band& g, int s) {
 // CHUNK panels per fused update: 8 for wide blocks (many tile columns), else 4.
 // LOOK >= 2 is required: G1 issues panel s-1's update of tile (s+1, s+1) on
 // its own, so that tile must never be part of a chunk.
-STBTA_DEV int look(const Band& g) { return g.nbt >= 24 ? 2 : 3; }
-STBTA_DEV int chunk_k(const Band& g) { return g.nbt >= 24 ? 8 : 4; }
+STBTA_DEV int look(const Band& g) { return g.look > 0 ? g.look : (g.nbt >= 24 ? 2 : 3); }
+STBTA_DEV int chunk_k(const Band& g) { return g.chunk > 0 ? g.chunk : (g.nbt >= 24 ? 8 : 4); }
+STBTA_DEV bool remainder_chunks(const Band& g) {
+  return g.remainder >= 0 ? g.remainder != 0 : g.nbt >= 24;
+}
 STBTA_DEV int chunk_first(const Band& g, int p) {
   const int t = p / g.nbt, j = p - t * g.nbt;
   return t * g.nbt + (j / chunk_k(g)) * chunk_k(g);
@@ -150,7 +153,7 @@ STBTA_DEV bool cross_col(const Band& g, int p, int C) {
 STBTA_DEV int col_mode(const Band& g, int p, int C) {
   if (p >= g.n * g.nbt) return 1;
   if (cross_col(g, p, C)) return chunk_last(g, p) ? 2 : 0;
-  if (C <= p + look(g) || g.nbt < 24) return 1;
+  if (C <= p + look(g) || !remainder_chunks(g)) return 1;
   return p == C - look(g) - 1 ? 2 : 0;
 }
 
@@ -717,6 +720,13 @@ static Band make_band(const double* const* regions, int n, int b, int a, int use
     g.tp = const_cast<double*>(regions[3]);
     g.data = g.dg;
   }
+  // tuning overrides (experiments; defaults by block width in look / chunk_k)
+  static const int env_chunk = [] { const char* v = getenv("STBTA_CHUNK"); return v ? atoi(v) : 0; }();
+  static const int env_look = [] { const char* v = getenv("STBTA_LOOK"); return v ? atoi(v) : 0; }();
+  static const int env_rem = [] { const char* v = getenv("STBTA_REMAINDER"); return v ? atoi(v) : -1; }();
+  g.chunk = env_chunk;
+  g.look = env_look >= 2 ? env_look : 0;  // LOOK >= 2 is required (G1)
+  g.remainder = env_rem;
   const bool base16 = al16(g.dg) && (n < 2 || al16(g.lw)) && (a == 0 || al16(g.ar));
   g.vec_b = base16 && (ldb % 2 == 0);
   g.vec_a = g.vec_b && (a % 2 == 0) && (a == 0 || al16(g.tp));
