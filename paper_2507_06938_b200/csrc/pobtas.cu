@@ -11,8 +11,7 @@
 //      previous / next time block and of its own block) through a 4-stage
 //      cp.async ring of 32-column (32-row) slices -- the factor is read
 //      exactly once per sweep at HBM rate, prefetched before the dependency's
-//      solution is even ready (the ring holds a whole dependency, so the
-//      latest one is resident when its flag arrives);
+//      solution is even ready;
 //   2. folds each dependency's solution in, in a fixed order (deterministic),
 //      as soon as that tile publishes it (acquire flag);
 //   3. solves its 128x128 diagonal triangle in 32-row blocks (warp-level
@@ -28,10 +27,9 @@ namespace stbta {
 
 constexpr int PS_NT = 256;
 constexpr int NR = 8;      // right-hand sides per sweep launch
-constexpr int SL = 16;     // slice width
-constexpr int PST = 9;     // ring stages: a whole 128-wide dependency (8 slices) in flight, so
-                           // the one folded right after its flag (R-2) is already resident
-constexpr int F_LD = SL;               // forward slice: 128 rows x SL cols, 16-byte chunks swizzled
+constexpr int SL = 32;     // slice width
+constexpr int PST = 4;     // ring stages
+constexpr int F_LD = SL;               // forward slice: 128 rows x 32 cols, 16-byte chunks swizzled
 constexpr int B_LD = 128;              // backward slice: 32 rows x 128 cols (read along rows)
 constexpr int STAGE = 128 * F_LD > SL * B_LD ? 128 * F_LD : SL * B_LD;
 // forward slice element (r, q): chunk (q >> 1) of row r stored at chunk (q >> 1) ^ (r & 7), so
@@ -39,9 +37,8 @@ constexpr int STAGE = 128 * F_LD > SL * B_LD ? 128 * F_LD : SL * B_LD;
 STBTA_DEV int fsw(int r, int q) { return r * F_LD + ((((q >> 1) ^ (r & 7))) << 1) + (q & 1); }
 constexpr int P_LD = 129;              // coupling block in shared memory
 constexpr int WPK = 128 * 129 / 2;     // packed lower 128 x 128
-constexpr int PB_DOUBLES = PST * STAGE > 128 * P_LD ? PST * STAGE : 128 * P_LD;
-constexpr int PS_SMEM_DOUBLES = WPK + PB_DOUBLES + 128 * NR + 128 * NR;
-static_assert(PS_SMEM_DOUBLES * 8 <= 227 * 1024, "sweep shared memory exceeds 227 KB");
+constexpr int PS_SMEM_DOUBLES = WPK + 128 * P_LD + 128 * NR + 128 * NR;
+static_assert(PST * STAGE <= 128 * P_LD, "ring must fit in the coupling-block region");
 
 STBTA_DEV int pk(int r, int c) { return r * (r + 1) / 2 + c; }
 
@@ -88,7 +85,7 @@ __global__ void __launch_bounds__(PS_NT, 1) inv_tiles_kernel(Band g, double* win
   }
 }
 
-// One SL-wide slice of dependency tile k into a ring stage (16-byte copies
+// One 32-wide slice of dependency tile k into a ring stage (16-byte copies
 // when the rows are 16-byte aligned, zero fill outside the tile).
 template <bool FWD>
 STBTA_DEV void load_slice(double* ring_st, const Band& g, int R, int k, int sl, int extR,
@@ -101,7 +98,7 @@ STBTA_DEV void load_slice(double* ring_st, const Band& g, int R, int k, int sl, 
     const bool vec = ((uintptr_t)t.p % 16 == 0) && (t.ld % 2 == 0);
     if (vec) {
       for (int e = tid; e < 128 * SL / 2; e += PS_NT) {
-        const int r = e / (SL / 2), q = (e % (SL / 2)) * 2;
+        const int r = e >> 4, q = (e & 15) * 2;
         int bytes = 0;
         const double* src = t.p;
         if (r < extR && c0 + q < extK) {
@@ -112,7 +109,7 @@ STBTA_DEV void load_slice(double* ring_st, const Band& g, int R, int k, int sl, 
       }
     } else {
       for (int e = tid; e < 128 * SL; e += PS_NT) {
-        const int r = e / SL, q = e % SL;
+        const int r = e >> 5, q = e & 31;
         const bool ok = r < extR && c0 + q < extK;
         cp_async8(ring_st + fsw(r, q), ok ? t.p + (long long)r * t.ld + c0 + q : t.p, ok);
       }
@@ -175,7 +172,7 @@ __global__ void __launch_bounds__(PS_NT, 1) sweep_kernel(SweepArgs p) {
   extern __shared__ __align__(16) double sm[];
   double* Wp = sm;                   // packed W of this tile
   double* Pb = Wp + WPK;             // ring for the pulled dependencies, then the push block
-  double* ybuf = Pb + PB_DOUBLES;    // dependency solution / this tile's solution, 128 x NR
+  double* ybuf = Pb + 128 * P_LD;    // dependency solution / this tile's solution, 128 x NR
   double* accb = ybuf + 128 * NR;    // right-hand side, 128 x NR
   double* ring = Pb;
   __shared__ int s_k;

@@ -12,7 +12,3 @@ for cfg in "4 3 0" "4 3 1" "8 3 0" "4 2 0" "6 3 0"; do
   echo "C2 chunk=$1 look=$2 rem=$3 $(STBTA_CHUNK=$1 STBTA_LOOK=$2 STBTA_REMAINDER=$3 timeout 300 python tools/prof_dag.py 48 2048 6 2>&1 | sed -n 2p)" >> $out
 done
 cat $out
-# POBTAS sweep breakdown (ring of a whole dependency)
-timeout 300 python tools/prof_solve.py 48 2048 6 > gpurun_out/r2_H_profsolve_c2.log 2>&1
-timeout 300 python tools/prof_solve.py 12 5026 3 > gpurun_out/r2_H_profsolve_c3.log 2>&1
-timeout 600 python -m pytest tests/test_gpu_solver.py tests/test_gpu_dist.py -m gpu -q -x 2>&1 | tail -3 > gpurun_out/r2_H_pytest.log
