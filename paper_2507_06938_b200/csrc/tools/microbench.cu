@@ -2,7 +2,7 @@
 // of the solver path): the UPDATE tile product in isolation, per CTA shape.
 #include "../../../include/stbta_tools.h"
 #include "../potrf_tile.cuh"
-#include "../tile_mma.cuh"
+#include "mma_variants.cuh"
 
 namespace stbta {
 
