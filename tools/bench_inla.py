@@ -3,6 +3,10 @@
   python tools/bench_inla.py c1            # univariate mode finding (full run)
   python tools/bench_inla.py c3            # one trivariate f_obj at theta0
   python tools/bench_inla.py c4 [depth]    # the 31-task gradient batch at theta0 on all GPUs
+  python tools/bench_inla.py c3post        # fd_hessian (451 f_obj) + latent marginals at the C3 mode
+
+(The C3 mode search itself: tools/c3_fit.py; the per-iteration north-star
+number: bench.py.)
 
 Inputs come from the reference generators restated in
 paper_2507_06938_b200/synthetic.py (same seeds and draw order).  Prints one
@@ -115,61 +119,6 @@ def c4(depth=1):
     }), flush=True)
 
 
-def c3iter(max_iter=2, depth=1):
-    """C3 north star: seconds per L-BFGS iteration (Armijo line search on GPU 0
-    + the 31-point central-difference gradient over every visible GPU)."""
-    G = torch.cuda.device_count()
-    t0 = time.perf_counter()
-    data, prior = _c3_evaluator()
-    evs = [inla.ObjectiveEvaluator(data.spec, prior=prior, device=torch.device("cuda", g))
-           for g in range(G)]
-    setup = time.perf_counter() - t0
-    runner = sched.GpuRunner(evs, depth=depth)
-    th = np.array(TRI_THETA0)
-    runner.evaluate_points([th] * G)  # warm every device
-    inla.prior_cache_clear()
-    recs = []
-    t0 = time.perf_counter()
-    with warnings.catch_warnings():
-        warnings.simplefilter("ignore")
-        res = inla.minimize(evs[0], th, gtol=1e-3, ftol=1e-12, max_iter=max_iter, runner=runner,
-                            on_iteration=recs.append)
-    total = time.perf_counter() - t0
-    print(json.dumps({
-        "config": f"C3 trivariate n_s=1675 n_t=48: L-BFGS iterations from theta0, gradient over {G} GPUs",
-        "n_gpus": G, "setup_s": setup, "iterations": res.iterations, "total_s_incl_first_gradient": total,
-        "s_per_iteration": [r.seconds for r in recs], "f": res.f,
-        "f_evals_per_iteration": [r.f_evals for r in recs] if hasattr(recs[0], "f_evals") else None,
-    }), flush=True)
-
-
-def c3fit(max_iter=60):
-    """C3 full hyperparameter optimisation (BASELINE configs[2]): minimize from
-    theta0 to convergence with the gradient over every visible GPU."""
-    G = torch.cuda.device_count()
-    data, prior = _c3_evaluator()
-    evs = [inla.ObjectiveEvaluator(data.spec, prior=prior, device=torch.device("cuda", g))
-           for g in range(G)]
-    runner = sched.GpuRunner(evs)
-    th = np.array(TRI_THETA0)
-    runner.evaluate_points([th] * G)
-    inla.prior_cache_clear()
-    recs = []
-    t0 = time.perf_counter()
-    with warnings.catch_warnings():
-        warnings.simplefilter("ignore")
-        res = inla.minimize(evs[0], th, gtol=1e-3, ftol=1e-12, max_iter=max_iter, runner=runner,
-                            on_iteration=recs.append)
-    total = time.perf_counter() - t0
-    print(json.dumps({
-        "config": f"C3 trivariate full mode search from theta0 over {G} GPUs (gtol 1e-3, ftol 1e-12)",
-        "n_gpus": G, "iterations": res.iterations, "status": res.status, "f_evals": res.f_evals,
-        "total_s": total, "s_per_iteration": [r.seconds for r in recs],
-        "tries_per_iteration": [r.f_evals - 31 for r in recs],
-        "theta_star": res.theta.tolist(), "f_star": res.f, "theta_true": TRI_TRUE,
-    }), flush=True)
-
-
 def c3post():
     """C3 after the mode search (BASELINE configs[2]): the
     finite-difference Hessian at the mode (1 + 2d + 2d(d-1) = 451 f_obj over
@@ -179,9 +128,9 @@ def c3post():
     evs = [inla.ObjectiveEvaluator(data.spec, prior=prior, device=torch.device("cuda", g))
            for g in range(G)]
     runner = sched.GpuRunner(evs)
-    with open(os.path.join(os.path.dirname(__file__), "..", "profiles",
-                           "r01_c3_full_fit_4gpu.json")) as fh:
-        th = np.array(json.load(fh)["theta_star"])
+    # the mode of the full C3 fit (tools/c3_fit.py: the last recorded BFGS state)
+    th = np.load(os.path.join(os.path.dirname(__file__), "..", "bench_data",
+                              "c3_bfgs_states.npz"))["theta"][-1]
     runner.evaluate_points([th] * G)
     inla.prior_cache_clear()
     t0 = time.perf_counter()
@@ -208,11 +157,7 @@ if __name__ == "__main__":
         c1()
     elif which == "c3":
         c3()
-    elif which == "c3fit":
-        c3fit(int(sys.argv[2]) if len(sys.argv) > 2 else 60)
     elif which == "c3post":
         c3post()
-    elif which == "c3iter":
-        c3iter(int(sys.argv[2]) if len(sys.argv) > 2 else 2)
     else:
         c4(int(sys.argv[2]) if len(sys.argv) > 2 else 1)
