@@ -53,6 +53,8 @@ struct SweepArgs {
   double* part;   // arrow partials [ntile][a][NR] (forward)
   const double* xtip;  // packed x_tip [a][NR] (backward)
   double* push;   // [ntile][128][NR]: coupling contribution pushed to the next tile
+  int* flags2;    // one per tile: its second-neighbour push is ready
+  double* push2;  // [ntile][128][NR]: coupling contribution pushed two tiles ahead
   unsigned long long* prof;  // optional debug timers (slots 20..23)
   const double* winv;  // [ntile][WPK]: packed inverses of the diagonal tiles
 };
@@ -197,17 +199,22 @@ __global__ void __launch_bounds__(PS_NT, 1) sweep_kernel(SweepArgs p) {
 
   // pulled dependencies: forward k in [lo, R-1) ascending; backward k in (R+1, hi] descending
   // (the adjacent tile is pushed: it sends its coupling product with its flag)
-  int kfirst, nk, crit;
+  // The two nearest tiles push: R-1 (R+1 backward) with its flag, R-2 (R+2)
+  // right after its flag -- so the tile folded latest is R-3, three periods
+  // before R publishes, and the pulled fold leaves the sweep's recurrence.
+  int kfirst, nk, crit, crit2;
   if (FWD) {
     const int lo = max(0, (i - 1) * g.nbt);
     kfirst = lo;
-    nk = max(0, R - 1 - lo);
     crit = R - 1;  // -1 for the first tile
+    crit2 = (R - 2 >= lo) ? R - 2 : -1;
+    nk = max(0, R - 1 - lo) - (crit2 >= 0 ? 1 : 0);
   } else {
     const int hi = min((i + 2) * g.nbt, p.ntile) - 1;
     kfirst = hi;
-    nk = max(0, hi - R - 1);
     crit = (R + 1 < p.ntile) ? R + 1 : -1;
+    crit2 = (R + 2 <= hi) ? R + 2 : -1;
+    nk = max(0, hi - R - 1) - (crit2 >= 0 ? 1 : 0);
   }
   auto dep = [&](int d) { return FWD ? kfirst + d : kfirst - d; };
   auto nsl = [&](int k) { return (tile_extent(g, k) + SL - 1) / SL; };
@@ -310,6 +317,18 @@ __global__ void __launch_bounds__(PS_NT, 1) sweep_kernel(SweepArgs p) {
 #pragma unroll
     for (int c = 0; c < NRC; ++c) accb[r * NR + c] += (r < extR && c < nc) ? acc[c] : 0.0;
   }
+  // the second neighbour's pushed contribution (ready a period earlier)
+  if (crit2 >= 0) {
+    if (tid == 0) {
+      while (ld_acquire(p.flags2 + crit2) == 0) __nanosleep(10);
+    }
+    __syncthreads();
+    if (h == 0) {
+      const double* u = p.push2 + (long long)R * 128 * NR;
+#pragma unroll
+      for (int c = 0; c < NRC; ++c) accb[r * NR + c] -= (r < extR && c < nc) ? __ldcg(u + r * NR + c) : 0.0;
+    }
+  }
   // the adjacent (critical) tile's pushed contribution
   if (crit >= 0) {
     if (tid == 0) {
@@ -375,6 +394,58 @@ __global__ void __launch_bounds__(PS_NT, 1) sweep_kernel(SweepArgs p) {
       atomicAdd(p.prof + 23, t3 - t2);
     }
   }
+  // off the critical step: the second-neighbour push, straight from global
+  // memory (forward u = L_{R+2,R} y_R to R+2; backward v = L_{R,R-2}^T x_R to R-2)
+  int to2 = -1;
+  if (FWD) {
+    if (R + 2 < p.ntile && R >= max(0, ((R + 2) / g.nbt - 1) * g.nbt)) to2 = R + 2;
+  } else {
+    if (R - 2 >= 0 && R <= min(((R - 2) / g.nbt + 2) * g.nbt, p.ntile) - 1) to2 = R - 2;
+  }
+  if (to2 >= 0) {
+    double* dst = p.push2 + (long long)to2 * 128 * NR;
+    if (FWD) {  // stage L_{R+2,R} in the (free) push-block buffer, then the 128-row gemv
+      const TilePtr t = tile_ptr(g, R + 2, R);
+      const int nr = tile_extent(g, R + 2);
+      for (int e = tid; e < 128 * 128; e += PS_NT) {  // row layout of the push block
+        const int rr = e >> 7, cc = e & 127;
+        const bool ok = rr < nr && cc < extR;
+        cp_async8(Pb + rr * P_LD + cc, ok ? t.p + (long long)rr * t.ld + cc : t.p, ok);
+      }
+      cp_async_commit();
+      cp_async_wait<0>();
+      __syncthreads();
+      gemv128<NRC>(accb, ybuf, accb, [&](int rr, int q) { return Pb[rr * P_LD + q]; });
+      for (int e = tid; e < 128 * NR; e += PS_NT) dst[e] = accb[e];
+    } else {  // thread per output column (coalesced rows), halves over the rows
+      const TilePtr t = tile_ptr(g, R, R - 2);
+      const int ncl = tile_extent(g, R - 2);
+      double sacc[NRC];
+#pragma unroll
+      for (int c = 0; c < NRC; ++c) sacc[c] = 0.0;
+      if (r < ncl)
+        for (int rr = h * 64; rr < min(extR, h * 64 + 64); ++rr) {
+          const double m = __ldcg(t.p + (long long)rr * t.ld + r);
+#pragma unroll
+          for (int c = 0; c < NRC; ++c) sacc[c] = fma(m, ybuf[rr * NR + c], sacc[c]);
+        }
+      double* tmp = accb;  // accb is no longer needed
+      if (h == 1) {
+#pragma unroll
+        for (int c = 0; c < NRC; ++c) tmp[r * NR + c] = sacc[c];
+      }
+      __syncthreads();
+      if (h == 0) {
+#pragma unroll
+        for (int c = 0; c < NRC; ++c) dst[r * NR + c] = sacc[c] + tmp[r * NR + c];
+      }
+    }
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence();
+      atomicExch(p.flags2 + R, 1);
+    }
+  }
 }
 
 // mode 0 (forward): y_tip = L_tip^-1 (r_tip - sum_R part[R]);  mode 1: x_tip = L_tip^-T y_tip.
@@ -416,33 +487,37 @@ static size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 
 struct PobtasWs {
   int* flags;
+  int* flags2;
   int* ticket;
   double* part;
   double* xtip;
   double* push;
+  double* push2;
   double* winv;
 };
 
 static size_t pobtas_ws(int n, int b, int a, char* base, PobtasWs* o) {
   const int ntile = n * ((b + 127) / 128);
-  const size_t f = align_up((size_t)(ntile + 2) * sizeof(int));
+  const size_t f = align_up((size_t)(2 * ntile + 2) * sizeof(int));
   const size_t pa = align_up((size_t)ntile * (a > 0 ? a : 1) * NR * sizeof(double));
   const size_t xt = align_up((size_t)(a > 0 ? a : 1) * NR * sizeof(double));
-  const size_t pu = align_up((size_t)ntile * 128 * NR * sizeof(double));
+  const size_t pu = align_up((size_t)ntile * 128 * NR * sizeof(double));  // push and push2
   const size_t wi = (size_t)ntile * WPK * sizeof(double);
   if (o) {
     o->flags = reinterpret_cast<int*>(base);
-    o->ticket = o->flags + ntile;
+    o->flags2 = o->flags + ntile;
+    o->ticket = o->flags + 2 * ntile;
     o->part = reinterpret_cast<double*>(base + f);
     o->xtip = reinterpret_cast<double*>(base + f + pa);
     o->push = reinterpret_cast<double*>(base + f + pa + xt);
-    o->winv = reinterpret_cast<double*>(base + f + pa + xt + pu);
+    o->push2 = reinterpret_cast<double*>(base + f + pa + xt + pu);
+    o->winv = reinterpret_cast<double*>(base + f + pa + xt + 2 * pu);
   }
-  return f + pa + xt + pu + wi;
+  return f + pa + xt + 2 * pu + wi;
 }
 
 static int run_sweeps(SweepArgs p, int mode, const PobtasWs& ws, cudaStream_t st) {
-  const size_t fbytes = (size_t)(p.ntile + 1) * sizeof(int);  // flags + ticket
+  const size_t fbytes = (size_t)(2 * p.ntile + 1) * sizeof(int);  // flags, flags2, ticket
   const size_t smem = PS_SMEM_DOUBLES * sizeof(double);
   const size_t ismem = INV_SMEM_DOUBLES * sizeof(double);
   static std::atomic<unsigned long long> attr_mask{0};  // per device
@@ -547,6 +622,8 @@ int stbta_pobtas_ex(const double* diag, const double* lower, const double* arrow
   p.ntile = n * g.nbt;
   p.ldx = nrhs;
   p.flags = ws.flags;
+  p.flags2 = ws.flags2;
+  p.push2 = ws.push2;
   p.ticket = ws.ticket;
   p.part = ws.part;
   p.xtip = ws.xtip;
