@@ -16,9 +16,10 @@ device kernels:
   partition) are packed into one flat buffer; the root assembles the reduced
   2(P-1)-block BTA in partition order (bta_dist.py:322-350) and factorizes it
   by POBTAF.
-* ``d_solve`` is a Schur-complement solve: two interior POBTAS per partition
-  around one reduced solve, joined by the coupling products of
-  ``stbta_couple`` (device kernels, fixed summation order).
+* ``d_solve`` runs through the chain factor: one forward and one backward
+  interior POBTAS sweep per partition around one reduced solve, joined by
+  the factor's right-separator link and arrowhead rows in ``stbta_couple``
+  (device kernels, fixed summation order).
 * ``d_selected_invert`` seeds each chain's inverse with the reduced selected
   inverse (separator, fill and tip entries) and continues the POBTASI
   recursion over the interior (``stbta_pobtasi_ex`` with ``nstart``), which is
@@ -798,9 +799,10 @@ def _sep_solution(factor, red_x, p):
 
 
 def d_solve(factor, rhs, counter=None, phase_times=None):
-    """Partitioned solve (bta_dist.py:370-458) as a Schur-complement solve:
-    interior solves per partition, reduced separator solve, interior back
-    substitution; every coupling product runs in ``stbta_couple``."""
+    """Partitioned solve (bta_dist.py:370-458) through the chain factors: a
+    forward interior sweep per partition, the reduced separator solve, a
+    backward interior sweep; the factor's link / arrowhead couplings run in
+    ``stbta_couple``."""
     if factor.sequential is not None:
         with _phase(phase_times, "total"):
             return bta.solve(factor.sequential, rhs, counter=counter)
