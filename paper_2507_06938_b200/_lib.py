@@ -11,7 +11,9 @@ import os
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libstbta.so")
+# STBTA_LIB selects another build of the same ABI (the bounds-checked
+# libstbta_check.so of `make check`, for the checking runs)
+LIB_PATH = os.environ.get("STBTA_LIB") or os.path.join(_HERE, "libstbta.so")
 TOOLS_LIB_PATH = os.path.join(_HERE, "libstbta_tools.so")
 
 _lib = None

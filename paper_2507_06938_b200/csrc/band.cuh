@@ -70,6 +70,10 @@ STBTA_DEV TilePtr tile_ptr(const Band& g, int R, int C) {
   double* tip = g.tp;
   TilePtr t;
   const int NB = g.n * g.nbt;
+  // a tile of the lower band: C <= R < S; block tiles on the diagonal or
+  // first sub-diagonal block; arrow rows against any block column or the tip
+  STBTA_CHECK(C >= 0 && R >= C && R < g.S);
+  STBTA_CHECK(R >= NB || C >= NB || (R / g.nbt - C / g.nbt == 0 || R / g.nbt - C / g.nbt == 1));
   if (C >= NB) {  // tip
     const int qr = R - NB, qc = C - NB;
     t.p = tip + (long long)qr * TT * g.a + qc * TT;
@@ -95,6 +99,7 @@ STBTA_DEV TilePtr tile_ptr(const Band& g, int R, int C) {
 STBTA_DEV TilePtr tile_ptr_upper(const Band& g, int R, int C) {
   const long long b = g.ldb;
   const int NB = g.n * g.nbt;
+  STBTA_CHECK(R > C && R < g.S && ((R >= NB && C >= NB) || (R < NB && R / g.nbt == C / g.nbt)));
   if (C >= NB) {  // tip
     TilePtr p;
     p.p = g.tp + (long long)(C - NB) * TT * g.a + (R - NB) * TT;

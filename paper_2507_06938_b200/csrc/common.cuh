@@ -13,6 +13,25 @@
 
 #define STBTA_DEV __device__ __forceinline__
 
+// Device bounds checks of the checked build (make check -> libstbta_check.so,
+// -DSTBTA_CHECKS; loaded with STBTA_LIB=...): a violated invariant prints and
+// traps, so an out-of-region tile address fails loudly instead of reading or
+// writing a neighbour's storage.  Compiled out of the product library.
+#ifdef STBTA_CHECKS
+#include <cstdio>
+#define STBTA_CHECK(cond)                                                              \
+  do {                                                                                 \
+    if (!(cond)) {                                                                     \
+      printf("stbta check failed: %s (%s:%d)\n", #cond, __FILE__, __LINE__);            \
+      __trap();                                                                        \
+    }                                                                                  \
+  } while (0)
+#else
+#define STBTA_CHECK(cond) \
+  do {                    \
+  } while (0)
+#endif
+
 namespace stbta {
 
 // Kernel attributes (max dynamic shared memory) are per device: track, per

@@ -51,8 +51,10 @@ __global__ void __launch_bounds__(256) assemble_kernel(double* __restrict__ data
     for (int k = threadIdx.x; k < ASM_TILE; k += 256) tile[k] = 0.0;
     __syncthreads();
     const long long e0 = tile_start[ti], e1 = tile_start[ti + 1];
-    for (long long e = e0 + threadIdx.x; e < e1; e += 256)
+    for (long long e = e0 + threadIdx.x; e < e1; e += 256) {
+      STBTA_CHECK(t.offsets[e] >= base && t.offsets[e] - base < ASM_TILE && t.offsets[e] < nstore);
       tile[t.offsets[e] - base] = entry_value(t, e);
+    }
     __syncthreads();
     const long long len = min((long long)ASM_TILE, nstore - base);
     if (len == ASM_TILE) {
