@@ -55,6 +55,19 @@ METRIC = "BTA Cholesky/selinv FP64 TFLOP/s"
 UNIT = "TFLOP/s"
 
 
+def _hbm_gbs():
+    """Measured copy bandwidth of this pool's B200s (MEASURED_PEAKS.json), else
+    the B200_PROFILING.md fallback."""
+    try:
+        with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "MEASURED_PEAKS.json")) as fh:
+            return float(json.load(fh)["hbm_gbs"])
+    except (OSError, KeyError, ValueError):
+        return 6540.0
+
+
+HBM_GBS = _hbm_gbs()
+
+
 def parse_args():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
@@ -76,6 +89,10 @@ def parse_args():
     p.add_argument("--cpu-c3", action="store_true",
                    help="also time the reference CPU C3 f_obj in this arm (the --impl reference "
                         "arm does it by default at N=1)")
+    p.add_argument("--solve", default="w", choices=["w", "tile"],
+                   help="C2 step's POBTAS: w = block-inverse GEMVs sharing POBTASI's W pre-pass "
+                        "(stbta_pobtasi_prepare / stbta_pobtas_w / stbta_pobtasi_prepared), "
+                        "tile = the tile-sweep kernel with POBTASI computing W itself")
     p.add_argument("--no-inla", action="store_true",
                    help="skip the C3 north-star measurement (BFGS iterations over the N GPUs)")
     return p.parse_args()
@@ -585,7 +602,9 @@ def main():
     x = torch.empty_like(rhs0)
     inv = bta.BTAMatrix(n, b, a, torch.empty_like(pristine))
     ws_f = torch.empty(lib.stbta_pobtaf_workspace_bytes(n, b, a), dtype=torch.uint8, device=dev)
-    ws_s = torch.empty(lib.stbta_pobtas_workspace_bytes(n, b, a, 1), dtype=torch.uint8, device=dev)
+    use_w = args.solve == "w"
+    ws_s = torch.empty(lib.stbta_pobtas_w_workspace_bytes(n, b, a) if use_w else
+                       lib.stbta_pobtas_workspace_bytes(n, b, a, 1), dtype=torch.uint8, device=dev)
     ws_i = torch.empty(lib.stbta_pobtasi_workspace_bytes(n, b, a), dtype=torch.uint8, device=dev)
     ld = torch.zeros(2, dtype=torch.float64, device=dev)
     info = torch.zeros(1, dtype=torch.int32, device=dev)
@@ -603,15 +622,30 @@ def main():
                                     _lib.ptr(ws_f), ws_f.numel(), sp), "pobtaf")
         if evs:
             evs[1].record(stream)
-        x.copy_(rhs0)
-        _lib.check(lib.stbta_pobtas(_lib.ptr(mat.data), n, b, a, 1, _lib.ptr(x), 1, 0,
-                                    _lib.ptr(ws_s), ws_s.numel(), sp), "pobtas")
+        if use_w:  # W_t = L_tt^-1 once, shared by the solve and the selected inversion
+            _lib.check(lib.stbta_pobtasi_prepare(_lib.ptr(mat.data), n, b, a, _lib.ptr(ws_i),
+                                                 ws_i.numel(), sp), "pobtasi_prepare")
         if evs:
             evs[2].record(stream)
-        _lib.check(lib.stbta_pobtasi(_lib.ptr(mat.data), _lib.ptr(inv.data), n, b, a, 1,
-                                     _lib.ptr(ws_i), ws_i.numel(), sp), "pobtasi")
+        x.copy_(rhs0)
+        if use_w:
+            _lib.check(lib.stbta_pobtas_w(_lib.ptr(mat.data), n, b, a, 1, _lib.ptr(x), 1, 0,
+                                          _lib.ptr(ws_i), _lib.ptr(ws_s), ws_s.numel(), sp),
+                       "pobtas_w")
+        else:
+            _lib.check(lib.stbta_pobtas(_lib.ptr(mat.data), n, b, a, 1, _lib.ptr(x), 1, 0,
+                                        _lib.ptr(ws_s), ws_s.numel(), sp), "pobtas")
         if evs:
             evs[3].record(stream)
+        if use_w:
+            _lib.check(lib.stbta_pobtasi_prepared(_lib.ptr(mat.data), _lib.ptr(inv.data), None, n,
+                                                  b, a, 1, _lib.ptr(ws_i), ws_i.numel(), sp, None),
+                       "pobtasi_prepared")
+        else:
+            _lib.check(lib.stbta_pobtasi(_lib.ptr(mat.data), _lib.ptr(inv.data), n, b, a, 1,
+                                         _lib.ptr(ws_i), ws_i.numel(), sp), "pobtasi")
+        if evs:
+            evs[4].record(stream)
 
     for _ in range(args.warmup):
         step()
@@ -623,7 +657,7 @@ def main():
     clocks = ClockSampler(local)
     clocks.start()
     time.sleep(0.3)
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(args.steps)]
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -641,8 +675,9 @@ def main():
     clk = clocks.stop()
     elapsed = t_start.elapsed_time(t_end) * 1e-3
     t_f = sum(e[0].elapsed_time(e[1]) for e in evs) * 1e-3 / args.steps
-    t_s = sum(e[1].elapsed_time(e[2]) for e in evs) * 1e-3 / args.steps
-    t_i = sum(e[2].elapsed_time(e[3]) for e in evs) * 1e-3 / args.steps
+    t_w = sum(e[1].elapsed_time(e[2]) for e in evs) * 1e-3 / args.steps  # W pass (w mode)
+    t_s = sum(e[2].elapsed_time(e[3]) for e in evs) * 1e-3 / args.steps
+    t_i = t_w + sum(e[3].elapsed_time(e[4]) for e in evs) * 1e-3 / args.steps
     if world > 1:
         t = torch.tensor([elapsed], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -663,6 +698,8 @@ def main():
             m = bta.BTAMatrix(n, b, a, host_in)                  # pinned H2D upload
             fac = bta.factorize(m, use_arrow=True)                 # bta.py:177
             bta.logdet(fac)                                        # bta.py:238
+            if use_w:
+                bta.prepare_inverse(fac)                           # W shared by solve + selinv
             xs = bta.solve(fac, host_rhs)                          # bta.py:305 (host in/out)
             sel = bta.selected_invert(fac, out=host_out)           # bta.py:310, streamed to host
             sel.numpy(out=host_out)                                # waits for the D2H stream
@@ -742,8 +779,12 @@ def main():
                                         "(MEASURED_PEAKS.json has no FP64 entry)"},
             "routines": {
                 "pobtaf": {"ms": 1e3 * t_f, "tflops": f_f / t_f / 1e12},
-                "pobtas": {"ms": 1e3 * t_s, "gbs": perf.bytes_pobtas(n, b, a) / t_s / 1e9},
-                "pobtasi": {"ms": 1e3 * t_i, "tflops": f_i / t_i / 1e12},
+                "pobtas": {"ms": 1e3 * t_s, "gbs": perf.bytes_pobtas(n, b, a) / t_s / 1e9,
+                           "frac_hbm": perf.bytes_pobtas(n, b, a) / t_s / 1e9 / HBM_GBS,
+                           "kernel": "stbta_pobtas_w (block-inverse GEMVs, one cooperative "
+                                     "launch)" if use_w else "stbta_pobtas (tile sweeps)"},
+                "pobtasi": {"ms": 1e3 * t_i, "tflops": f_i / t_i / 1e12,
+                            "w_prepass_ms": 1e3 * t_w if use_w else None},
             },
             "logdet": logdet_dev,
             "gpu_launches": launches,

@@ -123,6 +123,29 @@ int stbta_pobtasi_stream_out(const double* factor, double* inv, double* host_out
                              int a, int has_arrow, void* workspace, size_t workspace_bytes,
                              void* stream, void* copy_stream);
 
+/* ------------------------------------------------ W-based POBTAS (solve) --
+ * The block inverses W_t = L_tt^-1 (and W_tip) that POBTASI computes first
+ * can be computed once per factor and shared between the triangular solves
+ * and the selected inversion:
+ *   stbta_pobtasi_prepare: W into a POBTASI workspace (stbta_pobtasi_workspace_bytes).
+ *   stbta_pobtas_w: same contract as stbta_pobtas (bta.solve / forward_substitute /
+ *     backward_substitute, bta.py:249-307) but each block step is a GEMV with W_t
+ *     (y_t = W_t (r_t - L_{t,t-1} y_{t-1}), x_t = W_t^T (...)) in one cooperative
+ *     kernel; si_workspace = the prepared POBTASI workspace, workspace of
+ *     stbta_pobtas_w_workspace_bytes.
+ *   stbta_pobtasi_prepared: stbta_pobtasi (host_out NULL) or
+ *     stbta_pobtasi_stream_out (host_out pinned) on a prepared workspace; skips
+ *     the W pre-pass. */
+int stbta_pobtasi_prepare(const double* factor, int n, int b, int a, void* workspace,
+                          size_t workspace_bytes, void* stream);
+size_t stbta_pobtas_w_workspace_bytes(int n, int b, int a);
+int stbta_pobtas_w(const double* factor, int n, int b, int a, int has_arrow, double* rhs,
+                   int nrhs, int mode, const void* si_workspace, void* workspace,
+                   size_t workspace_bytes, void* stream);
+int stbta_pobtasi_prepared(const double* factor, double* inv, double* host_out, int n, int b,
+                           int a, int has_arrow, void* workspace, size_t workspace_bytes,
+                           void* stream, void* copy_stream);
+
 /* ------------------------------------------------------ Q assembly / f_obj --
  * stbta_assemble: write the theta-dependent values of a precision matrix into
  * a BTA buffer of nstore elements, zero everywhere else.  Replaces the value

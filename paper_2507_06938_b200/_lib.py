@@ -66,6 +66,16 @@ _SIGNATURES = {
         c_int,
         [c_vp, c_int, c_int, c_int, c_int, c_vp, c_vp, c_vp, ctypes.c_uint, c_vp, c_size, c_vp],
     ),
+    "stbta_pobtasi_prepare": (c_int, [c_vp, c_int, c_int, c_int, c_vp, c_size, c_vp]),
+    "stbta_pobtasi_prepared": (
+        c_int,
+        [c_vp, c_vp, c_vp, c_int, c_int, c_int, c_int, c_vp, c_size, c_vp, c_vp],
+    ),
+    "stbta_pobtas_w_workspace_bytes": (c_size, [c_int, c_int, c_int]),
+    "stbta_pobtas_w": (
+        c_int,
+        [c_vp, c_int, c_int, c_int, c_int, c_vp, c_int, c_int, c_vp, c_vp, c_size, c_vp],
+    ),
     "stbta_pobtasi_stream_out": (
         c_int,
         [c_vp, c_vp, c_vp, c_int, c_int, c_int, c_int, c_vp, c_size, c_vp, c_vp],

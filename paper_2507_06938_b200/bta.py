@@ -18,6 +18,8 @@ There is no CPU fallback: without the library or a CUDA device every call
 raises :class:`~paper_2507_06938_b200._lib.StbtaError`.
 """
 
+import os
+
 import numpy as np
 import torch
 
@@ -296,6 +298,7 @@ class BTAFactor:
         self.logdet_dev = logdet_dev
         self.info_dev = info_dev
         self._logdet = None
+        self._si_ws = None  # POBTASI workspace holding W_t = L_tt^-1 (prepare_inverse)
 
     @property
     def dim(self):
@@ -397,19 +400,61 @@ def _as_device_rhs(factor, rhs):
     return x.contiguous(), host
 
 
-def _pobtas(factor, x, mode, counter=None, stream=None):
+def _solve_policy():
+    """STBTA_SOLVE: "tile" (POBTAS tile sweeps), "w" (block-inverse GEMVs,
+    preparing W when the factor has none) or "auto" (default: W when the
+    factor already holds it, tile sweeps otherwise)."""
+    v = os.environ.get("STBTA_SOLVE", "auto")
+    if v not in ("auto", "tile", "w"):
+        raise ValueError(f"STBTA_SOLVE={v!r}: expected auto, tile or w")
+    return v
+
+
+def prepare_inverse(factor, stream=None):
+    """Compute the block inverses W_t = L_tt^-1 (and W_tip) of `factor` once
+    (the first step of POBTASI) and keep them with the factor: later solves
+    then run as block GEMVs (``stbta_pobtas_w``) and :func:`selected_invert`
+    skips its own W pass.  Returns the workspace holding them."""
+    if factor._si_ws is None:
+        lib = _lib.load()
+        m = factor.matrix
+        n, b, a = m.n_blocks, m.block_size, m.arrow_size
+        with torch.cuda.device(m.device):
+            ws = _workspace(lib.stbta_pobtasi_workspace_bytes(n, b, a), m.device)
+            _lib.check(
+                lib.stbta_pobtasi_prepare(_lib.ptr(m.data), n, b, a, _lib.ptr(ws), ws.numel(),
+                                          _lib.stream_ptr(stream)),
+                "stbta_pobtasi_prepare",
+            )
+        factor._si_ws = ws
+    return factor._si_ws
+
+
+def _pobtas(factor, x, mode, counter=None, stream=None, policy=None):
     lib = _lib.load()
     m = factor.matrix
     n, b, a = m.n_blocks, m.block_size, m.arrow_size
     nrhs = 1 if x.dim() == 1 else int(x.shape[1])
-    ws = _workspace(lib.stbta_pobtas_workspace_bytes(n, b, a, nrhs), m.device)
-    _lib.check(
-        lib.stbta_pobtas(
-            _lib.ptr(m.data), n, b, a, int(bool(factor.has_arrow)), _lib.ptr(x), nrhs, mode,
-            _lib.ptr(ws), ws.numel(), _lib.stream_ptr(stream),
-        ),
-        "stbta_pobtas",
-    )
+    policy = policy or _solve_policy()
+    if policy == "w" or (policy == "auto" and factor._si_ws is not None):
+        si = prepare_inverse(factor, stream)
+        ws = _workspace(lib.stbta_pobtas_w_workspace_bytes(n, b, a), m.device)
+        _lib.check(
+            lib.stbta_pobtas_w(
+                _lib.ptr(m.data), n, b, a, int(bool(factor.has_arrow)), _lib.ptr(x), nrhs, mode,
+                _lib.ptr(si), _lib.ptr(ws), ws.numel(), _lib.stream_ptr(stream),
+            ),
+            "stbta_pobtas_w",
+        )
+    else:
+        ws = _workspace(lib.stbta_pobtas_workspace_bytes(n, b, a, nrhs), m.device)
+        _lib.check(
+            lib.stbta_pobtas(
+                _lib.ptr(m.data), n, b, a, int(bool(factor.has_arrow)), _lib.ptr(x), nrhs, mode,
+                _lib.ptr(ws), ws.numel(), _lib.stream_ptr(stream),
+            ),
+            "stbta_pobtas",
+        )
     if counter is not None:  # reference charges: b^2 per block and sweep, a^2 for the forward tip
         if mode in (0, 1):
             for _ in range(n):
@@ -456,24 +501,35 @@ def selected_invert(factor, counter=None, stream=None, out=None):
     n, b, a = m.n_blocks, m.block_size, m.arrow_size
     with torch.cuda.device(m.device):
         inv = BTAMatrix(n, b, a, torch.empty_like(m.data))
-        ws = _workspace(lib.stbta_pobtasi_workspace_bytes(n, b, a), m.device)
+        prepared = factor._si_ws is not None
+        ws = factor._si_ws if prepared else _workspace(lib.stbta_pobtasi_workspace_bytes(n, b, a), m.device)
         if (out is not None and isinstance(out, torch.Tensor) and not out.is_cuda and out.is_pinned()
                 and out.dtype == torch.float64 and out.numel() == inv._data.numel()
                 and out.is_contiguous() and stream is None):
             cs = _side_stream(m.device, "download")
+            fn = lib.stbta_pobtasi_prepared if prepared else lib.stbta_pobtasi_stream_out
             _lib.check(
-                lib.stbta_pobtasi_stream_out(
+                fn(
                     _lib.ptr(m.data), _lib.ptr(inv.data), out.data_ptr(), n, b, a,
                     int(bool(factor.has_arrow)), _lib.ptr(ws), ws.numel(), _lib.stream_ptr(None),
                     cs.cuda_stream,
                 ),
-                "stbta_pobtasi_stream_out",
+                "stbta_pobtasi_prepared" if prepared else "stbta_pobtasi_stream_out",
             )
             done = torch.cuda.Event()
             done.record(cs)
             inv._data.record_stream(cs)
             ws.record_stream(cs)
             inv._host_copy = (out, done)
+        elif prepared:
+            _lib.check(
+                lib.stbta_pobtasi_prepared(
+                    _lib.ptr(m.data), _lib.ptr(inv.data), None, n, b, a,
+                    int(bool(factor.has_arrow)), _lib.ptr(ws), ws.numel(), _lib.stream_ptr(stream),
+                    None,
+                ),
+                "stbta_pobtasi_prepared",
+            )
         else:
             _lib.check(
                 lib.stbta_pobtasi(

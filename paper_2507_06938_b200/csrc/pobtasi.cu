@@ -637,6 +637,338 @@ static TileJob job(double* C, long long ldc, int M, int N, double alpha) {
   return j;
 }
 
+// ------------------------------------------------ W-based solve (POBTAS)
+// With the block inverses W_t = L_tt^-1 at hand (the selected inversion's
+// pre-pass), the block triangular solves need no tile chain:
+//   forward   y_t = W_t (r_t - L_{t,t-1} y_{t-1})            t = 0 .. n-1
+//             y_tip = W_tip (r_tip - sum_t A_t y_t)
+//   backward  x_tip = W_tip^T y_tip
+//             x_t = W_t^T (y_t - L_{t+1,t}^T x_{t+1} - A_t^T x_tip)   t = n-1 .. 0
+// One persistent kernel (one CTA per SM, grid-wide barriers between the
+// phases) streams every block GEMV at HBM rate across all SMs: rows -> warps
+// for L y / W z (coalesced rows, warp sum), columns -> threads with row
+// chunks for the transposed products (coalesced, partial sums reduced in
+// chunk order).  Deterministic: every sum has a fixed order.
+constexpr int WS_NT = 512;
+constexpr int WS_NR = 8;          // right-hand sides per launch
+constexpr int WS_CHUNK = 64;      // rows per partial sum of a transposed product (default)
+constexpr int WS_CHUNK_MIN = 32;  // smallest chunk the workspace is sized for
+
+struct WsArgs {
+  const double *dg, *lw, *ar, *tp;  // factor regions (row stride b)
+  const double *W, *Wt;             // block inverses (lower), tip inverse
+  double* x;                        // rhs / solution (dim x nrhs, row-major)
+  double* z;                        // WS_NR x zld scratch (one contiguous vector per rhs)
+  double* part;                     // WS_NR x pld partial sums (chunk-major per rhs)
+  unsigned* bar;                    // grid barrier counter (zeroed)
+  long long zld, pld;
+  int n, b, a, arrow, mode, nrhs, ncols;
+  int chunk, colmap;                // transposed products: rows per partial; 1 = round robin
+  unsigned long long* prof;         // debug: per-phase ns (CTA 0) at prof[40 + phase]
+};
+
+STBTA_DEV unsigned long long ws_timer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+STBTA_DEV unsigned ld_acquire_u(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// all CTAs of the (co-resident, one per SM: cooperative launch) grid
+STBTA_DEV void grid_sync(unsigned* bar, unsigned& target) {
+  __syncthreads();
+  target += gridDim.x;
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(bar, 1u);
+    while (ld_acquire_u(bar) < target) __nanosleep(20);
+  }
+  __syncthreads();
+}
+
+// s[c] += sum_{j < len} row[j] * v[j * sj + c * sc], lane-strided, U row loads
+// in flight per lane (factor / W rows are read-only for the whole launch).
+template <int NRC, int U>
+STBTA_DEV void row_dot(const double* __restrict__ row, int len, const double* v, long long sj,
+                       long long sc, int nc, int lane, double (&s)[NRC]) {
+  for (int j0 = lane; j0 < len; j0 += 32 * U) {
+    double m[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) m[u] = (j0 + 32 * u < len) ? __ldg(row + j0 + 32 * u) : 0.0;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int j = j0 + 32 * u;
+      if (j < len) {
+#pragma unroll
+        for (int c = 0; c < NRC; ++c)
+          if (c < nc) s[c] = fma(m[u], v[j * sj + c * sc], s[c]);
+      }
+    }
+  }
+}
+
+// s[c] += sum_{i0 <= i < i1} M[i * ld + j] * v[i * sj + c * sc]: one column, U loads in flight
+template <int NRC, int U>
+STBTA_DEV void col_dot(const double* __restrict__ M, long long ld, int j, int i0, int i1,
+                       const double* v, long long sj, long long sc, int nc, double (&s)[NRC]) {
+  for (int i = i0; i < i1; i += U) {
+    double m[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) m[u] = (i + u < i1) ? __ldg(M + (long long)(i + u) * ld + j) : 0.0;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (i + u < i1) {
+#pragma unroll
+        for (int c = 0; c < NRC; ++c)
+          if (c < nc) s[c] = fma(m[u], v[(i + u) * sj + c * sc], s[c]);
+      }
+    }
+  }
+}
+
+// sum_{ch0 <= ch < ch1} pc[ch * b + j] in chunk order, 16 loads in flight
+STBTA_DEV double sum_chunks(const double* pc, long long b, int j, int ch0, int ch1) {
+  double acc = 0.0;
+  for (int ch = ch0; ch < ch1; ch += 16) {
+    double v[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) v[u] = (ch + u < ch1) ? pc[(long long)(ch + u) * b + j] : 0.0;
+#pragma unroll
+    for (int u = 0; u < 16; ++u) acc += v[u];
+  }
+  return acc;
+}
+
+template <int NRC, int U, int UC>
+__global__ void __launch_bounds__(WS_NT, 1) wsolve_kernel(WsArgs p) {
+  const int tid = threadIdx.x, lane = tid & 31;
+  // warp-level work items (a row, or 32 columns of one row chunk) go round
+  // robin over the CTAs (item = blockIdx + grid * k), so triangular row
+  // lengths and the W^T chunks' triangle spread evenly over the SMs
+  const int nwarp = gridDim.x * (WS_NT / 32);
+  const int gw = blockIdx.x + gridDim.x * (tid >> 5);
+  const long long b = p.b, bb = b * b;
+  const int a = p.a, n = p.n, ldx = p.nrhs, nc = p.ncols;
+  const long long tipr = (long long)n * b;  // first tip row of x
+  const long long zld = p.zld, pld = p.pld;
+  const int njb = (p.b + 31) / 32;
+  unsigned target = 0;
+  const int CH = p.chunk;
+  const int nch = (p.b + CH - 1) / CH;
+  // column work item k -> (chunk, column j) of this lane, or j = b when idle
+  const int ncw = p.colmap ? nch * njb : (nch * (int)b + WS_NT - 1) / WS_NT * (WS_NT / 32);
+  double* const z = p.z;
+  double* const part = p.part;
+  int nwt = 0;  // W^T items on / below the diagonal
+  for (int ch = 0; ch < nch; ++ch) nwt += min(njb, (ch * CH + CH + 31) / 32);
+  unsigned long long tl = (p.prof && blockIdx.x == 0 && tid == 0) ? ws_timer() : 0;
+#define WS_SYNC(k)                                                \
+  do {                                                            \
+    grid_sync(p.bar, target);                                     \
+    if (p.prof && blockIdx.x == 0 && tid == 0) {                  \
+      const unsigned long long now_ = ws_timer();                 \
+      p.prof[40 + (k)] += now_ - tl;                              \
+      tl = now_;                                                  \
+    }                                                             \
+  } while (0)
+
+  if (p.mode != 2) {  // ------------------------------------------ forward
+    for (int t = 0; t < n; ++t) {
+      // z = r_t - L_{t,t-1} y_{t-1}
+      for (int i = gw; i < b; i += nwarp) {
+        double s[NRC];
+#pragma unroll
+        for (int c = 0; c < NRC; ++c) s[c] = 0.0;
+        if (t > 0)
+          row_dot<NRC, U>(p.lw + (long long)(t - 1) * bb + (long long)i * b, (int)b,
+                          p.x + (long long)(t - 1) * b * ldx, ldx, 1, nc, lane, s);
+#pragma unroll
+        for (int c = 0; c < NRC; ++c) {
+          const double v = warp_sum(s[c]);
+          if (lane == 0 && c < nc) z[c * zld + i] = p.x[((long long)t * b + i) * ldx + c] - v;
+        }
+      }
+      WS_SYNC(0);
+      // y_t = W_t z (lower triangle of W_t)
+      for (int i = gw; i < b; i += nwarp) {
+        double s[NRC];
+#pragma unroll
+        for (int c = 0; c < NRC; ++c) s[c] = 0.0;
+        row_dot<NRC, U>(p.W + (long long)t * bb + (long long)i * b, i + 1, z, 1, zld, nc, lane, s);
+#pragma unroll
+        for (int c = 0; c < NRC; ++c) {
+          const double v = warp_sum(s[c]);
+          if (lane == 0 && c < nc) p.x[((long long)t * b + i) * ldx + c] = v;
+        }
+      }
+      WS_SYNC(1);
+    }
+    if (a > 0) {
+      // arrow partials part[c][t * a + r] = A_t[r] . y_t (warp per (t, r)), then the tip on CTA 0
+      if (p.arrow) {
+        for (int w = gw; w < n * a; w += nwarp) {
+          const int t = w / a, r = w % a;
+          double s[NRC];
+#pragma unroll
+          for (int c = 0; c < NRC; ++c) s[c] = 0.0;
+          row_dot<NRC, U>(p.ar + (long long)t * a * b + (long long)r * b, (int)b,
+                          p.x + (long long)t * b * ldx, ldx, 1, nc, lane, s);
+#pragma unroll
+          for (int c = 0; c < NRC; ++c) {
+            const double v = warp_sum(s[c]);
+            if (lane == 0 && c < nc) part[c * pld + w] = v;
+          }
+        }
+        WS_SYNC(2);
+      }
+      if (blockIdx.x == 0) {  // y_tip = W_tip (r_tip - sum_t part[t]): CTA 0, warp per tip row
+        const int wc = tid >> 5;
+        for (int r = wc; r < a; r += WS_NT / 32)
+          for (int c = 0; c < nc; ++c) {
+            double acc = 0.0;
+            if (p.arrow)
+              for (int t = lane; t < n; t += 32) acc += part[c * pld + (long long)t * a + r];
+            acc = warp_sum(acc);
+            if (lane == 0) z[c * zld + r] = p.x[(tipr + r) * ldx + c] - acc;
+          }
+        __syncthreads();
+        for (int r = wc; r < a; r += WS_NT / 32)
+          for (int c = 0; c < nc; ++c) {
+            double acc = 0.0;
+            for (int q = lane; q <= r; q += 32) acc = fma(p.Wt[(long long)r * a + q], z[c * zld + q], acc);
+            acc = warp_sum(acc);
+            if (lane == 0) p.x[(tipr + r) * ldx + c] = acc;
+          }
+      }
+      WS_SYNC(3);
+    }
+  }
+  if (p.mode == 1) return;
+  // -------------------------------------------------------------- backward
+  if (a > 0) {  // x_tip = W_tip^T y_tip: CTA 0, warp per tip row
+    if (blockIdx.x == 0) {
+      const int wc = tid >> 5;
+      for (int q = tid; q < a; q += WS_NT)
+        for (int c = 0; c < nc; ++c) z[c * zld + q] = p.x[(tipr + q) * ldx + c];
+      __syncthreads();
+      for (int r = wc; r < a; r += WS_NT / 32)
+        for (int c = 0; c < nc; ++c) {
+          double acc = 0.0;
+          for (int q = r + lane; q < a; q += 32) acc = fma(p.Wt[(long long)q * a + r], z[c * zld + q], acc);
+          acc = warp_sum(acc);
+          if (lane == 0) p.x[(tipr + r) * ldx + c] = acc;
+        }
+    }
+    WS_SYNC(4);
+  }
+  const int gt = blockIdx.x * WS_NT + tid;
+  for (int t = n - 1; t >= 0; --t) {
+    // partials of L_{t+1,t}^T x_{t+1}: item (row chunk, 32 columns)
+    if (t < n - 1) {
+      const double* L = p.lw + (long long)t * bb;  // block (t+1, t): rows of t+1, cols of t
+      const double* xn = p.x + (long long)(t + 1) * b * ldx;
+      for (int k = p.colmap ? gw : gt / 32; k < ncw; k += nwarp) {
+        int ch, j;
+        if (p.colmap) {
+          ch = k / njb;
+          j = (k % njb) * 32 + lane;
+        } else {
+          const int job = k * 32 + lane;
+          ch = job / (int)b;
+          j = job % (int)b;
+          if (ch >= nch) continue;
+        }
+        if (j >= b) continue;
+        double s[NRC];
+#pragma unroll
+        for (int c = 0; c < NRC; ++c) s[c] = 0.0;
+        col_dot<NRC, UC>(L, b, j, ch * CH, min((int)b, ch * CH + CH), xn, ldx, 1, nc, s);
+#pragma unroll
+        for (int c = 0; c < NRC; ++c)
+          if (c < nc) part[c * pld + (long long)ch * b + j] = s[c];
+      }
+      WS_SYNC(5);
+    }
+    // z = y_t - sum_chunks part - A_t^T x_tip (32-column items round robin over the CTAs)
+    for (int k = gw; k < njb; k += nwarp) {
+      const int j = k * 32 + lane;
+      if (j >= b) continue;
+      double s[NRC];
+#pragma unroll
+      for (int c = 0; c < NRC; ++c) s[c] = (c < nc) ? p.x[((long long)t * b + j) * ldx + c] : 0.0;
+      if (t < n - 1)
+#pragma unroll
+        for (int c = 0; c < NRC; ++c)
+          if (c < nc) s[c] -= sum_chunks(part + c * pld, b, j, 0, nch);
+      if (p.arrow)
+        for (int r = 0; r < a; ++r) {
+          const double m = p.ar[(long long)t * a * b + (long long)r * b + j];
+#pragma unroll
+          for (int c = 0; c < NRC; ++c)
+            if (c < nc) s[c] = fma(-m, p.x[(tipr + r) * ldx + c], s[c]);
+        }
+#pragma unroll
+      for (int c = 0; c < NRC; ++c)
+        if (c < nc) z[c * zld + j] = s[c];
+    }
+    WS_SYNC(6);
+    // partials of W_t^T z: x_t[j] = sum_{i >= j} W_t[i][j] z[i]
+    {
+      // only the items on / below the diagonal (chunk ch: column blocks
+      // jb < nact(ch)), enumerated densely so they spread evenly
+      const double* Wb = p.W + (long long)t * bb;
+      for (int k = gw; k < nwt; k += nwarp) {
+        int ch = 0, r = k;
+        while (r >= min(njb, (ch * CH + CH + 31) / 32)) r -= min(njb, (ch * CH + CH + 31) / 32), ++ch;
+        const int j = r * 32 + lane;
+        if (j >= b || ch * CH + CH <= j) continue;  // above the diagonal: no partial
+        double s[NRC];
+#pragma unroll
+        for (int c = 0; c < NRC; ++c) s[c] = 0.0;
+        col_dot<NRC, UC>(Wb, b, j, max(ch * CH, j), min((int)b, ch * CH + CH), z, 1, zld, nc, s);
+#pragma unroll
+        for (int c = 0; c < NRC; ++c)
+          if (c < nc) part[c * pld + (long long)ch * b + j] = s[c];
+      }
+    }
+    WS_SYNC(7);
+    for (int k = gw; k < njb; k += nwarp) {
+      const int j = k * 32 + lane;
+      if (j >= b) continue;
+      double s[NRC];
+#pragma unroll
+      for (int c = 0; c < NRC; ++c) s[c] = 0.0;
+#pragma unroll
+      for (int c = 0; c < NRC; ++c)  // chunks above j's own hold no partial
+        if (c < nc) s[c] = sum_chunks(part + c * pld, b, j, j / CH, nch);
+#pragma unroll
+      for (int c = 0; c < NRC; ++c)
+        if (c < nc) p.x[((long long)t * b + j) * ldx + c] = s[c];
+    }
+    WS_SYNC(8);
+  }
+}
+#undef WS_SYNC
+
+// workspace: barrier | z (WS_NR x zld) | part (WS_NR x pld)
+static void wsolve_ld(int n, int b, int a, long long* zld, long long* pld) {
+  const long long nch = (b + WS_CHUNK_MIN - 1) / WS_CHUNK_MIN;
+  const long long rows = nch * b > (long long)n * a ? nch * b : (long long)n * a;
+  *zld = ((b > a ? b : a) + 31) / 32 * 32;
+  *pld = (rows + 31) / 32 * 32;
+}
+
+static size_t wsolve_ws_bytes(int n, int b, int a) {
+  long long zld, pld;
+  wsolve_ld(n, b, a, &zld, &pld);
+  return 256 + (size_t)(zld + pld) * WS_NR * sizeof(double);
+}
+
 }  // namespace stbta
 
 using namespace stbta;
@@ -663,7 +995,7 @@ int stbta_pobtasi(const double* factor, double* inv, int n, int b, int a, int ha
 static int pobtasi_impl(const double* Ld, const double* Ll, const double* La, const double* Lt,
                         double* Xd, double* Xl, double* Xa, double* Xt, int n, int b, int a,
                         int has_arrow, int nstart, void* workspace, size_t workspace_bytes,
-                        void* stream, cudaEvent_t ctr_ready, int* persistent);
+                        void* stream, cudaEvent_t ctr_ready, int* persistent, int w_ready = 0);
 
 int stbta_pobtasi_ex(const double* Ld, const double* Ll, const double* La, const double* Lt,
                      double* Xd, double* Xl, double* Xa, double* Xt, int n, int b, int a,
@@ -673,9 +1005,20 @@ int stbta_pobtasi_ex(const double* Ld, const double* Ll, const double* La, const
                       workspace_bytes, stream, nullptr, nullptr);
 }
 
+static int stream_out_impl(const double* factor, double* inv, double* host_out, int n, int b,
+                           int a, int has_arrow, void* workspace, size_t workspace_bytes,
+                           void* stream, void* copy_stream, int w_ready);
+
 int stbta_pobtasi_stream_out(const double* factor, double* inv, double* host_out, int n, int b,
                              int a, int has_arrow, void* workspace, size_t workspace_bytes,
                              void* stream, void* copy_stream) {
+  return stream_out_impl(factor, inv, host_out, n, b, a, has_arrow, workspace, workspace_bytes,
+                         stream, copy_stream, 0);
+}
+
+static int stream_out_impl(const double* factor, double* inv, double* host_out, int n, int b,
+                           int a, int has_arrow, void* workspace, size_t workspace_bytes,
+                           void* stream, void* copy_stream, int w_ready) {
   if (factor == nullptr || inv == nullptr || host_out == nullptr || n < 1 || b < 1 || a < 0)
     return STBTA_EARG;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
@@ -689,7 +1032,7 @@ int stbta_pobtasi_stream_out(const double* factor, double* inv, double* host_out
   int persistent = 0;
   e = pobtasi_impl(factor, factor + o_low, factor + o_arr, factor + o_tip, inv, inv + o_low,
                    inv + o_arr, inv + o_tip, n, b, a, has_arrow, -1, workspace, workspace_bytes,
-                   stream, memops().ok ? ev : nullptr, &persistent);
+                   stream, memops().ok ? ev : nullptr, &persistent, w_ready);
   if (e) {
     cudaEventDestroy(ev);
     return e;
@@ -726,12 +1069,129 @@ int stbta_pobtasi_stream_out(const double* factor, double* inv, double* host_out
   return 0;
 }
 
+
+static int prepare_w(const double* Ld, const double* Lt, int nw, int b, int a, bool tip,
+                     const PobtasiWs& ws, cudaStream_t st);
+
+int stbta_pobtasi_prepare(const double* factor, int n, int b, int a, void* workspace,
+                          size_t workspace_bytes, void* stream) {
+  if (factor == nullptr || workspace == nullptr || n < 1 || b < 1 || a < 0) return STBTA_EARG;
+  if (workspace_bytes < stbta_pobtasi_workspace_bytes(n, b, a)) return STBTA_EWORKSPACE;
+  PobtasiWs ws;
+  pobtasi_ws(n, b, a, reinterpret_cast<char*>(workspace), &ws);
+  const long long bb = (long long)b * b;
+  const double* tip = factor + (2LL * n - 1) * bb + (long long)n * a * b;
+  return prepare_w(factor, tip, n, b, a, true, ws, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int stbta_pobtasi_prepared(const double* factor, double* inv, double* host_out, int n, int b,
+                           int a, int has_arrow, void* workspace, size_t workspace_bytes,
+                           void* stream, void* copy_stream) {
+  if (factor == nullptr || inv == nullptr) return STBTA_EARG;
+  if (host_out != nullptr)
+    return stream_out_impl(factor, inv, host_out, n, b, a, has_arrow, workspace, workspace_bytes,
+                           stream, copy_stream, 1);
+  const long long bb = (long long)b * b;
+  const long long o_low = (long long)n * bb, o_arr = o_low + (long long)(n - 1) * bb;
+  const long long o_tip = o_arr + (long long)n * a * b;
+  return pobtasi_impl(factor, factor + o_low, factor + o_arr, factor + o_tip, inv, inv + o_low,
+                      inv + o_arr, inv + o_tip, n, b, a, has_arrow, -1, workspace,
+                      workspace_bytes, stream, nullptr, nullptr, 1);
+}
+
+size_t stbta_pobtas_w_workspace_bytes(int n, int b, int a) {
+  if (n < 1 || b < 1 || a < 0) return 0;
+  return wsolve_ws_bytes(n, b, a);
+}
+
+int stbta_pobtas_w(const double* factor, int n, int b, int a, int has_arrow, double* rhs,
+                   int nrhs, int mode, const void* si_workspace, void* workspace,
+                   size_t workspace_bytes, void* stream) {
+  if (factor == nullptr || rhs == nullptr || si_workspace == nullptr || workspace == nullptr ||
+      n < 1 || b < 1 || a < 0 || nrhs < 1 || mode < 0 || mode > 2)
+    return STBTA_EARG;
+  if (workspace_bytes < wsolve_ws_bytes(n, b, a)) return STBTA_EWORKSPACE;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  PobtasiWs si;
+  pobtasi_ws(n, b, a, reinterpret_cast<char*>(const_cast<void*>(si_workspace)), &si);
+  const long long bb = (long long)b * b;
+  char* base = reinterpret_cast<char*>(workspace);
+  WsArgs p{};
+  p.dg = factor;
+  p.lw = factor + (long long)n * bb;
+  p.ar = p.lw + (long long)(n - 1) * bb;
+  p.tp = p.ar + (long long)n * a * b;
+  p.W = si.Wall;
+  p.Wt = si.Wt;
+  p.bar = reinterpret_cast<unsigned*>(base);
+  wsolve_ld(n, b, a, &p.zld, &p.pld);
+  p.z = reinterpret_cast<double*>(base + 256);
+  p.part = p.z + (size_t)p.zld * WS_NR;
+  p.n = n; p.b = b; p.a = a;
+  p.arrow = (has_arrow && a > 0) ? 1 : 0;
+  p.mode = mode;
+  p.nrhs = nrhs;
+  p.chunk = b <= 3072 ? WS_CHUNK_MIN : WS_CHUNK;  // measured: C2 (b 2048) 32, C3 (b 5025) 64
+  p.colmap = 1;
+  p.prof = debug_profile();
+  int uw = 32;  // loads in flight per lane (single right-hand side)
+  if (const char* v = getenv("STBTA_WS_U")) uw = atoi(v);
+  if (const char* v = getenv("STBTA_WS_CHUNK")) p.chunk = atoi(v) >= WS_CHUNK_MIN ? atoi(v) : p.chunk;
+  if (const char* v = getenv("STBTA_WS_COLMAP")) p.colmap = atoi(v) ? 1 : 0;
+  const int grid = sm_count();
+  for (int c0 = 0; c0 < nrhs; c0 += WS_NR) {
+    p.x = rhs + c0;
+    p.ncols = nrhs - c0 < WS_NR ? nrhs - c0 : WS_NR;
+    int e = zero_async(p.bar, sizeof(unsigned), st);
+    if (e) return e;
+    void* args[] = {&p};
+    const void* fn = (const void*)wsolve_kernel<WS_NR, 4, 4>;
+    if (p.ncols == 1)
+      fn = uw >= 32 ? (const void*)wsolve_kernel<1, 16, 32> : (const void*)wsolve_kernel<1, 16, 16>;
+    e = (int)cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(WS_NT), args, 0, st);
+    count_launch();
+    if (e) return e;
+  }
+  return 0;
+}
+
 }  // extern "C"
+
+// W_i = L_ii^-1 for blocks i < nw (and W_tip when `tip`) into the workspace
+// (diagonal tiles in-CTA, then the off-diagonal tile diagonals).
+static int prepare_w(const double* Ld, const double* Lt, int nw, int b, int a, bool tip,
+                     const PobtasiWs& ws, cudaStream_t st) {
+  static std::atomic<unsigned long long> attr_mask{0};  // per device
+  const size_t smem = SI_SMEM_DOUBLES * sizeof(double);
+  int e;
+  if (attr_pending(attr_mask)) {
+    if ((e = (int)cudaFuncSetAttribute(inv_diag_tiles_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))) return e;
+    if ((e = (int)cudaFuncSetAttribute(inv_offdiag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))) return e;
+    attr_mark(attr_mask);
+  }
+  InvSet s{};
+  s.L = Ld; s.W = ws.Wall; s.Lt = Lt; s.Wt = ws.Wt;
+  s.n = nw; s.b = b; s.a = a; s.tmp = ws.tmp;
+  s.ntb = (b + 127) / 128;
+  const int nta = (a > 0 && tip) ? (a + 127) / 128 : 0;
+  const int nm = nw + ((a > 0 && tip) ? 1 : 0);
+  const int ntm = s.ntb > nta ? s.ntb : nta;
+  if (a > 0 && tip && (e = zero_async(ws.Wt, (size_t)a * a * sizeof(double), st))) return e;
+  inv_diag_tiles_kernel<<<dim3(ntm, nm), SI_NT, smem, st>>>(s);
+  count_launch();
+  if ((e = (int)cudaGetLastError())) return e;
+  for (int d = 1; d < ntm; ++d) {
+    inv_offdiag_kernel<<<dim3(ntm - d, nm), SI_NT, smem, st>>>(s, d);
+    count_launch();
+    if ((e = (int)cudaGetLastError())) return e;
+  }
+  return 0;
+}
 
 static int pobtasi_impl(const double* Ld, const double* Ll, const double* La, const double* Lt,
                         double* Xd, double* Xl, double* Xa, double* Xt, int n, int b, int a,
                         int has_arrow, int nstart, void* workspace, size_t workspace_bytes,
-                        void* stream, cudaEvent_t ctr_ready, int* persistent) {
+                        void* stream, cudaEvent_t ctr_ready, int* persistent, int w_ready) {
   if (Ld == nullptr || Xd == nullptr || n < 1 || b < 1 || a < 0 || nstart > n) return STBTA_EARG;
   if ((n > 1 && (Ll == nullptr || Xl == nullptr)) ||
       (a > 0 && (La == nullptr || Lt == nullptr || Xa == nullptr || Xt == nullptr)))
@@ -756,23 +1216,9 @@ static int pobtasi_impl(const double* Ld, const double* Ll, const double* La, co
   }
   if (nstart == 0) return 0;
 
-  // ---- 1. all inverses W_i (and W_tip) up front
-  InvSet s{};
-  s.L = Ld; s.W = ws.Wall; s.Lt = Lt; s.Wt = ws.Wt;
-  s.n = nstart; s.b = b; s.a = a; s.tmp = ws.tmp;
-  s.ntb = (b + 127) / 128;
-  const int nta = (a > 0 && full) ? (a + 127) / 128 : 0;
-  const int nm = nstart + ((a > 0 && full) ? 1 : 0);
-  const int ntm = s.ntb > nta ? s.ntb : nta;
-  if (a > 0 && full && (e = zero_async(ws.Wt, (size_t)a * a * sizeof(double), st))) return e;
-  inv_diag_tiles_kernel<<<dim3(ntm, nm), SI_NT, smem, st>>>(s);
-  count_launch();
-  if ((e = (int)cudaGetLastError())) return e;
-  for (int d = 1; d < ntm; ++d) {
-    inv_offdiag_kernel<<<dim3(ntm - d, nm), SI_NT, smem, st>>>(s, d);
-    count_launch();
-    if ((e = (int)cudaGetLastError())) return e;
-  }
+  // ---- 1. all inverses W_i (and W_tip) up front (already in the workspace
+  // when a W-based solve of the same factor prepared them)
+  if (!(w_ready && full) && (e = prepare_w(Ld, Lt, nstart, b, a, full, ws, st))) return e;
 
   if (a > 0 && !arrow && (e = zero_async(Xa, (size_t)nstart * a * b * sizeof(double), st)))
     return e;
