@@ -26,6 +26,10 @@ int stbta_debug_tile_bench(int variant, const double* A, const double* B, double
  * (6 u64) receives CTA 0's phase times in ns. */
 int stbta_debug_potrf_bench(const double* A, double* out, int reps, int grid,
                             unsigned long long* ph, void* stream);
+/* Cross-SM flag round trips from CTA 0 to every other CTA (one per SM, `reps`
+ * each; flags: 64 * SMs zeroed ints): out[4k..4k+3] = ping written (CTA 0
+ * %globaltimer), ping seen (CTA k), pong seen (CTA 0), smid of k. */
+int stbta_debug_timer_skew(int reps, int* flags, long long* out, void* stream);
 /* clock cycles of `iters` dependent DMMA (which=0) or DFMA (1) on one warp. */
 int stbta_debug_latency(int which, int iters, double* scratch, long long* cycles, void* stream);
 /* DMMA throughput with shared-memory fragment loads (mode 0 LDS.64, 1 LDS.128,
