@@ -640,6 +640,7 @@ class ObjectiveEvaluator:
             ws.data.copy_(self.assembly.unpad(padded))
             del padded
             factor = bta.factorize(ws, use_arrow=self.assembly.cond_has_arrow)
+            bta.prepare_inverse(factor)  # W shared by the mean solve and the selected inversion
             if self.n_observations:
                 rhs = torch.empty(self.spec.joint_dim, dtype=torch.float64, device=dev)
                 tau_d = torch.from_numpy(np.asarray(taus, dtype=np.float64)).to(dev)
