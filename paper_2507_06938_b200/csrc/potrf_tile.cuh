@@ -16,7 +16,7 @@ namespace stbta {
 
 constexpr int PT_LD = 129;   // row stride of the tile in shared memory
 constexpr int PT_WLD = 33;   // row stride of 32x32 blocks in shared memory
-constexpr int PT_SMEM_DOUBLES = 128 * PT_LD + 4 * 32 * PT_WLD + 256;
+constexpr int PT_SMEM_DOUBLES = 128 * PT_LD + 4 * 32 * PT_WLD + 128 + 144;
 
 // 8x8 DMMA fragments of up to U independent output tiles, interleaved so the
 // accumulator chains overlap: c[u] += sum_k A(m_u + g, k) * B(k, n_u + g').
@@ -130,9 +130,25 @@ STBTA_DEV void named_bar_sync(int id, int nthreads) {
 //   role 2: identity rows, lane = row: the result is e_lane L_kk^-T, which is
 //           row `lane` of W_kk^T -- the diagonal-block inverse for the TRSM
 //           tasks, at no extra latency.
-// All roles run the same column step; the pivot column of the diagonal block
-// is broadcast through smem (colbuf, 128 doubles) under a named barrier over
-// the `nthr` factor threads.  Returns false on a non-positive pivot.
+// Two pivot columns per step.  With column j (cb0) and column j+1 (cb1, not
+// yet updated by j) of the diagonal block:
+//   rs0 = 1/sqrt(d0), l1 = L[j+1][j] = cb0[j+1] rs0, d1 = cb1[j+1] - l1^2,
+//   rs1 = 1/sqrt(d1), L[i][j] = r_i[j] rs0, L[i][j+1] = (r_i[j+1] - L[i][j] l1) rs1,
+//   and the rank-2 trailing update of row i is, per column c,
+//   r_i[c] -= A_i cb0[c] + B_i cb1[c],  A_i = L[i][j] rs0 - B_i l1 rs0,  B_i = L[i][j+1] rs1.
+// Producer / consumer: only the diagonal warp (role 0) runs the pivot chain,
+// from its own registers (shuffles), and publishes each step -- cb0, cb1 and
+// the scalars rs0, rs1, l1 -- into one of two smem buffers (colbuf + 72 k,
+// k = step & 1) with bar.arrive on FULL[k] (named barrier 1 + k); the other
+// factor warps wait there, apply the step to their rows and release the buffer
+// with bar.arrive on EMPTY[k] (3 + k), which the producer waits on before it
+// refills it two steps later.  The pivot chain no longer waits for every
+// warp's 30-column update; the arithmetic (and so every bit) is unchanged.
+// `nthr` = 32 x factor warps.  Returns false on a non-positive pivot.
+STBTA_DEV void named_bar_arrive(int id, int nthreads) {
+  asm volatile("bar.arrive %0, %1;\n" ::"r"(id), "r"(nthreads) : "memory");
+}
+
 STBTA_DEV bool factor_col32(double* T, int k0, int row0, int role, double* WTb, double* colbuf,
                             double* dinv, double* ld_acc, int nthr) {
   const int lane = threadIdx.x & 31;
@@ -147,30 +163,20 @@ STBTA_DEV bool factor_col32(double* T, int k0, int row0, int role, double* WTb, 
   }
   bool ok = true;
   double mydiag = 1.0;
-  // Two pivot columns per broadcast round.  With column j (cb0) and column
-  // j+1 (cb1, not yet updated by j) of the diagonal block published:
-  //   rs0 = 1/sqrt(d0), l1 = L[j+1][j] = cb0[j+1] rs0, d1 = cb1[j+1] - l1^2,
-  //   rs1 = 1/sqrt(d1), L[i][j] = r_i[j] rs0, L[i][j+1] = (r_i[j+1] - L[i][j] l1) rs1,
-  //   and the rank-2 trailing update of row i is, per column c,
-  //   r_i[c] -= A_i cb0[c] + B_i cb1[c],  A_i = L[i][j] rs0 - B_i l1 rs0,  B_i = L[i][j+1] rs1
-  // (two FMAs per column pair, like the rank-1 form, half the rounds).
-#pragma unroll 16
-  for (int j = 0; j < 32; j += 2) {
-    double* cb0 = colbuf + ((j >> 1) & 1) * 64;
-    double* cb1 = cb0 + 32;
-    if (role == 0) {  // unscaled columns j, j+1 of the diagonal block
-      cb0[lane] = r[j];
-      cb1[lane] = r[j + 1];
-    }
-    named_bar_sync(1, nthr);
-    const double d0 = cb0[j];
-    const double rs0 = rsqrt_nr(d0);
-    const double l1 = cb0[j + 1] * rs0;
-    const double d1 = fma(-l1, l1, cb1[j + 1]);
-    const double rs1 = rsqrt_nr(d1);
-    const double lj0 = r[j] * rs0;                    // L[row][j]
-    const double lj1 = fma(-lj0, l1, r[j + 1]) * rs1;  // L[row][j+1]
-    if (role == 0) {
+  if (role == 0) {
+#pragma unroll
+    for (int j = 0; j < 32; j += 2) {
+      const int k = (j >> 1) & 1;
+      double* buf = colbuf + 72 * k;
+      const double d0 = __shfl_sync(0xffffffffu, r[j], j);
+      const double c01 = __shfl_sync(0xffffffffu, r[j], j + 1);
+      const double d1r = __shfl_sync(0xffffffffu, r[j + 1], j + 1);
+      const double rs0 = rsqrt_nr(d0);
+      const double l1 = c01 * rs0;
+      const double d1 = fma(-l1, l1, d1r);
+      const double rs1 = rsqrt_nr(d1);
+      const double lj0 = r[j] * rs0;
+      const double lj1 = fma(-lj0, l1, r[j + 1]) * rs1;
       ok = ok && (d0 > 0.0) && (d1 > 0.0);
       if (lane == j) {
         dinv[j] = rs0;
@@ -180,13 +186,40 @@ STBTA_DEV bool factor_col32(double* T, int k0, int row0, int role, double* WTb, 
         dinv[j + 1] = rs1;
         mydiag = lj1;
       }
+      if (j >= 4) named_bar_sync(3 + k, nthr);  // consumers are done with this buffer
+      buf[lane] = r[j];
+      buf[32 + lane] = r[j + 1];
+      if (lane == 0) {
+        buf[64] = rs0;
+        buf[65] = rs1;
+        buf[66] = l1;
+      }
+      named_bar_arrive(1 + k, nthr);
+      __syncwarp();
+      r[j] = lj0;
+      r[j + 1] = lj1;
+      const double B = lj1 * rs1;
+      const double A = fma(-B, l1, lj0) * rs0;
+#pragma unroll
+      for (int c = j + 2; c < 32; ++c) r[c] = fma(-A, buf[c], fma(-B, buf[32 + c], r[c]));
     }
-    r[j] = lj0;
-    r[j + 1] = lj1;
-    const double B = lj1 * rs1;
-    const double A = fma(-B, l1, lj0) * rs0;
-#pragma unroll 30
-    for (int c = j + 2; c < 32; ++c) r[c] = fma(-A, cb0[c], fma(-B, cb1[c], r[c]));
+  } else {
+#pragma unroll
+    for (int j = 0; j < 32; j += 2) {
+      const int k = (j >> 1) & 1;
+      const double* buf = colbuf + 72 * k;
+      named_bar_sync(1 + k, nthr);
+      const double rs0 = buf[64], rs1 = buf[65], l1 = buf[66];
+      const double lj0 = r[j] * rs0;
+      const double lj1 = fma(-lj0, l1, r[j + 1]) * rs1;
+      r[j] = lj0;
+      r[j + 1] = lj1;
+      const double B = lj1 * rs1;
+      const double A = fma(-B, l1, lj0) * rs0;
+#pragma unroll
+      for (int c = j + 2; c < 32; ++c) r[c] = fma(-A, buf[c], fma(-B, buf[32 + c], r[c]));
+      if (j < 28) named_bar_arrive(3 + k, nthr);
+    }
   }
   if (role == 2) {
 #pragma unroll
@@ -258,7 +291,7 @@ STBTA_DEV int potrf_tile_smem(double* T, double* WT, double* scratch, double* lo
   static_assert(NT == 256, "potrf_tile_smem is laid out for 8 warps");
   const int tid = threadIdx.x, warp = tid >> 5;
   double* dinv = scratch;          // 128: 1 / L_ii
-  double* colbuf = scratch + 128;  // 128: two pivot columns, double-buffered
+  double* colbuf = scratch + 128;  // 2 x 72: pivot column pair + scalars, double-buffered
   double ld_acc = 0.0;
   unsigned long long tp = (ph && tid == 0) ? pt_timer() : 0;
   auto stamp = [&](int k) {
