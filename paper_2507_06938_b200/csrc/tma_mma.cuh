@@ -132,21 +132,28 @@ STBTA_DEV void tile_mma_tma(double (&acc)[Cfg::MF][Cfg::NF][2], const TmaOpnd& A
     const double* as = base + s * TMA_STAGE;
     const double* bs = as + TMA_OPND;
     if (full) {
-#pragma unroll
-      for (int ks = 0; ks < 8; ++ks) {
+      // fragments double-buffered in registers: k-step ks+1's loads are
+      // issued before k-step ks's DMMAs, so their latency is off the pipe
+      double af[2][MF], bf[2][NF];
+      auto frag_load = [&](int ks, int b) {
         const int kp = tma_kp(ks, o4);
-        double af[MF], bf[NF];
 #pragma unroll
-        for (int i = 0; i < MF; ++i) af[i] = as[tma_off<false>(wm0 + i * 8 + gq, kp)];
+        for (int i = 0; i < MF; ++i) af[b][i] = as[tma_off<false>(wm0 + i * 8 + gq, kp)];
 #pragma unroll
         for (int j = 0; j < NF; ++j) {
           const double bv = bs[tma_off<false>(wn0 + j * 8 + gq, kp)];
-          bf[j] = NEG ? -bv : bv;
+          bf[b][j] = NEG ? -bv : bv;
         }
+      };
+      frag_load(0, 0);
+#pragma unroll
+      for (int ks = 0; ks < 8; ++ks) {
+        if (ks + 1 < 8) frag_load(ks + 1, (ks + 1) & 1);
 #pragma unroll
         for (int i = 0; i < MF; ++i)
 #pragma unroll
-          for (int j = 0; j < NF; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+          for (int j = 0; j < NF; ++j)
+            dmma884(acc[i][j][0], acc[i][j][1], af[ks & 1][i], bf[ks & 1][j]);
       }
     } else if (mfv > 0 && nfv > 0) {  // warp-uniform: only the wanted fragments
 #pragma unroll 1
@@ -253,18 +260,24 @@ STBTA_DEV void tile_mma_tma3(double (&acc)[Cfg::MF][Cfg::NF][2], const TmaOpnd3&
     const double* as = base + s * TMA_STAGE;
     const double* bs = as + TMA_OPND;
     if (full) {
+      // fragments double-buffered in registers (as tile_mma_tma)
+      double af[2][MF], bf[2][NF];
+      auto frag_load = [&](int ks, int b) {
+        const int kp = tma_kp(ks, o4);
+#pragma unroll
+        for (int i = 0; i < MF; ++i) af[b][i] = as[tma_off<AKM>(wm0 + i * 8 + gq, kp)];
+#pragma unroll
+        for (int j = 0; j < NF; ++j) bf[b][j] = bs[tma_off<BKM>(wn0 + j * 8 + gq, kp)];
+      };
+      frag_load(0, 0);
 #pragma unroll
       for (int ks = 0; ks < 8; ++ks) {
-        const int kp = tma_kp(ks, o4);
-        double af[MF], bf[NF];
-#pragma unroll
-        for (int i = 0; i < MF; ++i) af[i] = as[tma_off<AKM>(wm0 + i * 8 + gq, kp)];
-#pragma unroll
-        for (int j = 0; j < NF; ++j) bf[j] = bs[tma_off<BKM>(wn0 + j * 8 + gq, kp)];
+        if (ks + 1 < 8) frag_load(ks + 1, (ks + 1) & 1);
 #pragma unroll
         for (int i = 0; i < MF; ++i)
 #pragma unroll
-          for (int j = 0; j < NF; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+          for (int j = 0; j < NF; ++j)
+            dmma884(acc[i][j][0], acc[i][j][1], af[ks & 1][i], bf[ks & 1][j]);
       }
     } else if (mfv > 0 && nfv > 0) {  // warp-uniform: only the wanted fragments
 #pragma unroll 1
