@@ -459,7 +459,7 @@ __global__ void __launch_bounds__(DAG_NT, 1) pobtaf_dag_kernel(Band g, DagWs ws,
     potrf_worker(g, ws, info, smem);
     return;
   }
-  __shared__ unsigned long long s_tbars[TMA_ST];
+  __shared__ unsigned long long s_tbars[TMA_NBARS];
   tma_bars_init(s_tbars);
   unsigned tphase = 0;
 

@@ -443,7 +443,7 @@ constexpr int SIP_SMEM_DOUBLES =
 __global__ void __launch_bounds__(SI_NT, 1) sinv_persistent_kernel(SiParams P,
                                                                    const __grid_constant__ SiMaps maps) {
   extern __shared__ __align__(16) double smem[];
-  __shared__ unsigned long long s_tbars[TMA_ST];
+  __shared__ unsigned long long s_tbars[TMA_NBARS];
   tma_bars_init(s_tbars);
   unsigned tphase = 0;
   const TmaCtx tx{&maps, s_tbars, &tphase};

@@ -70,15 +70,22 @@ STBTA_DEV double* tma_stage_base(double* smem) {
 }
 
 // Call once per CTA before the first tile_mma_tma (thread 0 initialises).
+// bars[0, TMA_ST): stage full (TMA bytes landed); bars[TMA_ST, 2 TMA_ST):
+// stage consumed (one arrival per warp), which thread 0 waits on before it
+// refills the stage -- so the warps never meet at a CTA barrier per slab.
+constexpr int TMA_NBARS = 2 * TMA_ST;
 STBTA_DEV void tma_bars_init(unsigned long long* bars) {
   if (threadIdx.x == 0) {
     for (int s = 0; s < TMA_ST; ++s) mbar_init(bars + s, 1);
+    for (int s = 0; s < TMA_ST; ++s) mbar_init(bars + TMA_ST + s, blockDim.x >> 5);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
 }
 
-// `phase`: per-stage parity bits, identical in all threads, carried across calls.
+// `phase`: per-stage parity bits, identical in all threads, carried across
+// calls: bit s = full-barrier phase of stage s, bit 8 + s = uses of stage s
+// consumed so far (mod 2), i.e. the consumed-barrier phase.
 // Output rows >= mv / columns >= nv are not wanted by the caller: the warps'
 // 8 x 8 fragments lying entirely beyond them skip their loads and DMMAs
 // (partial last tiles, e.g. b = 5025 -> 33 columns, and the few arrow rows
@@ -127,8 +134,13 @@ STBTA_DEV void tile_mma_tma(double (&acc)[Cfg::MF][Cfg::NF][2], const TmaOpnd& A
     const int s = kt % TMA_ST;
     mbar_wait(bars + s, (phase >> s) & 1u);
     phase ^= 1u << s;
-    __syncthreads();  // every warp is done with the stage the next copy overwrites
-    if (tid == 0 && kt + TMA_ST - 1 < nk) issue(kt + TMA_ST - 1);
+    if (tid == 0 && kt + TMA_ST - 1 < nk) {
+      // the stage refilled now was consumed at kt - 1: wait until every warp
+      // has arrived on its consumed barrier (that use's phase completes)
+      const int sr = (kt + TMA_ST - 1) % TMA_ST;
+      if (kt >= 1) mbar_wait(bars + TMA_ST + sr, ((phase >> (8 + sr)) & 1u) ^ 1u);
+      issue(kt + TMA_ST - 1);
+    }
     const double* as = base + s * TMA_STAGE;
     const double* bs = as + TMA_OPND;
     if (full) {
@@ -176,6 +188,9 @@ STBTA_DEV void tile_mma_tma(double (&acc)[Cfg::MF][Cfg::NF][2], const TmaOpnd& A
         }
       }
     }
+    __syncwarp();  // the warp's reads of stage s are done (arrive releases them)
+    if (lane == 0) mbar_arrive(bars + TMA_ST + s);
+    phase ^= 1u << (8 + s);
   }
   __syncthreads();
 }
@@ -255,8 +270,13 @@ STBTA_DEV void tile_mma_tma3(double (&acc)[Cfg::MF][Cfg::NF][2], const TmaOpnd3&
     const int s = kt % TMA_ST;
     mbar_wait(bars + s, (phase >> s) & 1u);
     phase ^= 1u << s;
-    __syncthreads();
-    if (tid == 0 && kt + TMA_ST - 1 < nk) issue(kt + TMA_ST - 1);
+    if (tid == 0 && kt + TMA_ST - 1 < nk) {
+      // the stage refilled now was consumed at kt - 1: wait until every warp
+      // has arrived on its consumed barrier (that use's phase completes)
+      const int sr = (kt + TMA_ST - 1) % TMA_ST;
+      if (kt >= 1) mbar_wait(bars + TMA_ST + sr, ((phase >> (8 + sr)) & 1u) ^ 1u);
+      issue(kt + TMA_ST - 1);
+    }
     const double* as = base + s * TMA_STAGE;
     const double* bs = as + TMA_OPND;
     if (full) {
@@ -297,6 +317,9 @@ STBTA_DEV void tile_mma_tma3(double (&acc)[Cfg::MF][Cfg::NF][2], const TmaOpnd3&
         }
       }
     }
+    __syncwarp();  // the warp's reads of stage s are done (arrive releases them)
+    if (lane == 0) mbar_arrive(bars + TMA_ST + s);
+    phase ^= 1u << (8 + s);
   }
   __syncthreads();
 }
