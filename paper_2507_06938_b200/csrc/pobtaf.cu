@@ -619,17 +619,12 @@ __global__ void __launch_bounds__(DAG_NT, 1) pobtaf_dag_kernel(Band g, DagWs ws,
       // the C tile loads overlap the first operand slabs' copies
       auto cload = [&] { acc_load<Cfg128>(acc, tp.p, tp.ld, er, ec, 0, 0); };
       const TmaOpnd ta = tile_tma(g, tm, tk.R, tk.s0), tb = tile_tma(g, tm, tk.C, tk.s0);
-      const bool tma = ta.map != nullptr && tb.map != nullptr && (kw % 32 == 0 || ta.col + kw == g.b);
-      if (tma)
+      if (ta.map != nullptr && tb.map != nullptr && (kw % 32 == 0 || ta.col + kw == g.b))
         tile_mma_tma<Cfg128, true>(acc, ta, tb, kw, smem, s_tbars, tphase, cload, er, ec);
       else
         tile_mma<Cfg128, true>(acc, A, B, kw, 128, smem, 0, cload);
       if (ws.prof && tid == 0) atomicAdd(ws.prof + 22, gtimer() - t1);
-      const TmaOpnd tcm = tile_tma(g, tm, tk.R, tk.C);
-      if (tma && tcm.map != nullptr && er == 128 && ec == 128)
-        tile_store_tma<Cfg128>(acc, tcm, smem);  // full tile: bulk tensor stores
-      else
-        acc_store<Cfg128>(acc, tp.p, tp.ld, er, ec, 0, 0, 0, 1.0);
+      acc_store<Cfg128>(acc, tp.p, tp.ld, er, ec, 0, 0, 0, 1.0);
       __syncthreads();
       if (tid == 0) {
         __threadfence();

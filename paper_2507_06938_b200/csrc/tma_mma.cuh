@@ -195,50 +195,6 @@ STBTA_DEV void tile_mma_tma(double (&acc)[Cfg::MF][Cfg::NF][2], const TmaOpnd& A
   __syncthreads();
 }
 
-// Store a full 128 x 128 accumulator tile through the TMA engine (POBTAF
-// UPDATE epilogue): the warps stage their fragments in the (now idle) stage
-// ring in the operand layout -- four 32-wide slabs of two 16 x 128 boxes,
-// 128-byte swizzle -- and thread 0 issues eight bulk tensor stores to the
-// tile's place in its region and waits for their completion, so the 128 KB
-// leave the SM without occupying its load / store pipe.  Returns after a CTA
-// barrier with the tile written (the caller then fences and signals).
-STBTA_DEV void tma_store_2d(const CUtensorMap* map, int col, int row, const double* src) {
-  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];\n" ::"l"(
-                   reinterpret_cast<unsigned long long>(map)),
-               "r"(col), "r"(row), "r"(smem_u32(src))
-               : "memory");
-}
-
-template <class Cfg>
-STBTA_DEV void tile_store_tma(const double (&acc)[Cfg::MF][Cfg::NF][2], const TmaOpnd& C,
-                              double* smem) {
-  static_assert(Cfg::BM == 128 && Cfg::BN == 128, "TMA path is laid out for 128 x 128 tiles");
-  double* base = tma_stage_base(smem);
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int gq = lane >> 2, tq = lane & 3;
-  const int wm0 = (warp % Cfg::WARPS_M) * Cfg::WM;
-  const int wn0 = (warp / Cfg::WARPS_M) * Cfg::WN;
-#pragma unroll
-  for (int i = 0; i < Cfg::MF; ++i)
-#pragma unroll
-    for (int j = 0; j < Cfg::NF; ++j) {
-      const int r = wm0 + i * 8 + gq, c = wn0 + j * 8 + 2 * tq;
-      double* d = base + (c >> 5) * TMA_OPND + tma_off<false>(r, c & 31);
-      *reinterpret_cast<double2*>(d) = make_double2(acc[i][j][0], acc[i][j][1]);
-    }
-  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-  __syncthreads();
-  if (tid == 0) {
-#pragma unroll
-    for (int b = 0; b < 8; ++b)
-      tma_store_2d(C.map, C.col + b * 16, C.row, base + (b >> 1) * TMA_OPND + (b & 1) * TMA_HALF);
-    asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
-    asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
-    asm volatile("fence.proxy.async.global;\n" ::: "memory");
-  }
-  __syncthreads();
-}
-
 }  // namespace stbta
 
 // ---------------------------------------------------------------------------
