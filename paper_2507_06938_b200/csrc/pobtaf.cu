@@ -488,6 +488,19 @@ __global__ void __launch_bounds__(DAG_NT, 1) pobtaf_dag_kernel(Band g, DagWs ws,
     unsigned long long t0 = 0, t1 = 0;
     if (ws.prof != nullptr && tid == 0) t0 = gtimer();
 
+    // UPDATE: pull the C tile toward L2 while the dependencies are awaited, so
+    // the accumulator load after them does not pay the HBM latency (a stale
+    // copy is harmless: L2 is the point of coherence for the final writes)
+    if (tk.type == T_UPD) {
+      const TilePtr cp0 = tile_ptr(g, tk.R, tk.C);
+      const int er = tile_extent(g, tk.R), ec = tile_extent(g, tk.C);
+      const int lines = (ec * 8 + 127) / 128;  // 128-byte lines per row
+      for (int e = tid; e < er * lines; e += DAG_NT) {
+        const int r = e / lines, l = e - r * lines;
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(cp0.p + (long long)r * cp0.ld + l * 16));
+      }
+    }
+
     // ------------------------------------------------------ dependencies
     {
       const int* p = nullptr;
