@@ -348,7 +348,18 @@ STBTA_DEV bool potrf_worker(const Band& g, const DagWs& ws, int* info, double* s
     if (ws.prof != nullptr && tid == 0) t0 = gtimer();
     if (tid == 0) { s_ok = 1; s_fail = 0; }
     __syncthreads();
-    if (tid < NSTRIP && !spin_geq(counter(g, ws.ctr, s, tid, s), need(g, s, s), ws.abort_flag)) s_ok = 0;
+    // strips 0..NSTRIP-2 of the tile are loaded as soon as each is final (the
+    // STRIP tasks of one panel finish in strip order: strip q is 32(q+1)
+    // columns wide), overlapping the wait for the last one
+    double* T = smem;
+    const TilePtr tp = tile_ptr(g, s, s);
+    auto load_strip = [&](int q) {
+      const int warp = tid >> 5, lane = tid & 31;
+      for (int r = 32 * q + warp; r < min(w, 32 * q + 32); r += DAG_NT / 32) {
+        const double* src = tp.p + (long long)r * tp.ld;
+        for (int c = lane; c <= r; c += 32) cp_async8(T + r * PT_LD + c, src + c, true);
+      }
+    };
     if (tid == NSTRIP) {
       const unsigned long long tw0 = ws.prof ? gtimer() : 0;
       if (!wait_resident(g, ws, s)) s_ok = 0;
@@ -358,21 +369,16 @@ STBTA_DEV bool potrf_worker(const Band& g, const DagWs& ws, int* info, double* s
         tlp[11] = gtimer();
       }
     }
-    __syncthreads();
-    if (!s_ok) return false;
+    for (int q = 0; q < NSTRIP; ++q) {
+      if (tid == 0 && !spin_geq(counter(g, ws.ctr, s, q, s), need(g, s, s), ws.abort_flag)) s_ok = 0;
+      __syncthreads();
+      if (!s_ok) return false;
+      load_strip(q);
+    }
     if (ws.prof != nullptr && tid == 0) t1 = gtimer();
     {
-      double* T = smem;
       double* WT = T + 128 * PT_LD;
       double* scratch = WT + 4 * 32 * PT_WLD;
-      const TilePtr tp = tile_ptr(g, s, s);
-      {
-        const int warp = tid >> 5, lane = tid & 31;
-        for (int r = warp; r < w; r += DAG_NT / 32) {
-          const double* src = tp.p + (long long)r * tp.ld;
-          for (int c = lane; c <= r; c += 32) cp_async8(T + r * PT_LD + c, src + c, true);
-        }
-      }
       cp_async_commit();
       if (w < 128) {  // identity padding of a partial tile
         for (int e = tid; e < 128 * 128; e += DAG_NT) {
